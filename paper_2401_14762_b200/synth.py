@@ -1,0 +1,173 @@
+"""Frozen synthetic hyperspectral cubes for the BASELINE.json configs.
+
+The reference's datasets (Jasper Ridge, China, Salinas; `PAPER.md:35,69,106`)
+are not available here, so seeded synthetic cubes of the same shapes stand in
+for them.  The recipe is BASELINE.json's, frozen once (generator version
+``GENERATOR_VERSION``); the interpretation choices SURVEY.md §8(d) leaves open
+are fixed as follows and recorded in DESIGN.md:
+
+* "width" is the Gaussian sigma: bump = a * exp(-0.5 * ((b - c) / w)**2);
+* N(0, 0.01) is additive noise with sigma 0.01;
+* per pixel 1..4 bumps, centre U[0, B), width U[5, 40], amplitude U[0.1, 1];
+  a pixel always draws 4 bump parameter sets and zeroes the amplitudes of the
+  bumps past its count (so the random stream does not depend on the count);
+* clip to [0, 1]; coefficients c = C f with C the orthonormal DCT-II; entries
+  with |c| < 0.1 * max|c| (per pixel) are zeroed; the reference spectra are
+  f_s = Psi c_s with Psi = C^T (synthesis basis);
+* per-pixel mask: the M = floor(0.4 B + 0.5) smallest of B uniform keys,
+  sorted ascending (same M rule as `transform.py:131`);
+* y = f_s[mask];
+* the 2048x868 scaling cube tiles the 512x217 generator 4x4; tile (tx, ty)
+  uses seed ``base_seed + 4 * tx + ty``.
+
+This is the only place inputs are made; both the oracle and the GPU path
+consume the arrays it returns, so parity never depends on these choices.
+"""
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+GENERATOR_VERSION = "hcs-synth-v1"
+SAMPLE_RATIO = 0.4
+SPARSIFY_T = 0.1
+
+
+def dct_basis(n):
+    """Orthonormal synthesis basis Psi (n x n): f = Psi @ c, Psi = C^T with
+    C the orthonormal DCT-II, C[k, j] = s_k cos(pi k (2 j + 1) / (2 n)).
+
+    Built in closed form on the host in FP64; the same array is handed to the
+    oracle and to the GPU so basis rounding is identical on both sides.
+    """
+    if n < 1:
+        raise ValueError("basis size must be >= 1")
+    k = np.arange(n, dtype=np.int64)[:, None]
+    j = np.arange(n, dtype=np.int64)[None, :]
+    # exact integer range reduction of k (2j+1) modulo the period 4n keeps the
+    # cosine argument in [0, 2 pi) so the basis is orthonormal to ~1e-16
+    q = (k * (2 * j + 1)) % (4 * n)
+    # libm cosine over the 4n distinct angles (bit-stable across hosts of one
+    # image, unlike SIMD-dispatched np.cos)
+    table = np.array([math.cos(math.pi * i / (2.0 * n)) for i in range(4 * n)])
+    c = table[q] * math.sqrt(2.0 / n)
+    c[0, :] *= 1.0 / math.sqrt(2.0)
+    return np.ascontiguousarray(c.T)
+
+
+def measured_count(n, ratio=SAMPLE_RATIO):
+    """round-half-up(ratio * n), the reference's rule (`transform.py:131`)."""
+    return int(np.floor(ratio * n + 0.5))
+
+
+@dataclass
+class SyntheticCube:
+    """One synthetic measurement problem, pixel-major (x-major raster order).
+
+    basis        (n, n) float64 synthesis matrix Psi
+    coeffs       (P, n) float64 sparsified DCT coefficients (ground truth)
+    spectra      (P, n) float64 reference spectra f_s = Psi c (PSNR reference)
+    masks        (P, m) uint8 sorted measured band indices
+    y            (P, m) float64 measurements f_s[mask]
+    shape        (x, y) spatial shape, P = x * y
+    seeds        seeds used (one per tile)
+    """
+
+    basis: np.ndarray
+    coeffs: np.ndarray
+    spectra: np.ndarray
+    masks: np.ndarray
+    y: np.ndarray
+    shape: tuple
+    seeds: tuple
+    version: str = GENERATOR_VERSION
+
+    @property
+    def n(self):
+        return int(self.basis.shape[0])
+
+    @property
+    def m(self):
+        return int(self.masks.shape[1])
+
+    @property
+    def n_pixels(self):
+        return int(self.y.shape[0])
+
+
+def _tile(n_pix, n, basis, seed, chunk=1 << 16):
+    """Spectra, coefficients, masks and measurements for one seeded tile."""
+    rng = np.random.default_rng(seed)
+    m = measured_count(n)
+    counts = rng.integers(1, 5, size=n_pix)
+    centres = rng.uniform(0.0, float(n), size=(n_pix, 4))
+    widths = rng.uniform(5.0, 40.0, size=(n_pix, 4))
+    amps = rng.uniform(0.1, 1.0, size=(n_pix, 4))
+    amps[np.arange(4)[None, :] >= counts[:, None]] = 0.0
+    noise = rng.normal(0.0, 0.01, size=(n_pix, n))
+    keys = rng.random((n_pix, n))
+
+    bands = np.arange(n, dtype=np.float64)
+    coeffs = np.empty((n_pix, n))
+    spectra = np.empty((n_pix, n))
+    for lo in range(0, n_pix, chunk):
+        hi = min(n_pix, lo + chunk)
+        z = (bands[None, None, :] - centres[lo:hi, :, None]) / widths[lo:hi, :, None]
+        f = (amps[lo:hi, :, None] * np.exp(-0.5 * z * z)).sum(axis=1) + noise[lo:hi]
+        np.clip(f, 0.0, 1.0, out=f)
+        c = f @ basis                      # rows: c_p^T = f_p^T Psi  (c = Psi^T f)
+        mag = np.abs(c)
+        c[mag < SPARSIFY_T * mag.max(axis=1, keepdims=True)] = 0.0
+        coeffs[lo:hi] = c
+        spectra[lo:hi] = c @ basis.T       # f_s = Psi c
+    masks = np.sort(np.argpartition(keys, m - 1, axis=1)[:, :m], axis=1).astype(np.uint8)
+    y = np.take_along_axis(spectra, masks.astype(np.intp), axis=1)
+    return coeffs, spectra, masks, np.ascontiguousarray(y)
+
+
+def generate(x_dim, y_dim, n, seed=0, tiles=(1, 1)):
+    """Synthetic cube of shape (x_dim, y_dim, n), optionally tiled.
+
+    With tiles=(tx, ty) the cube is made of tx*ty independent tiles of size
+    (x_dim/tx, y_dim/ty), tile (i, j) seeded with seed + ty*i + j.
+    """
+    if n > 256:
+        raise ValueError("band indices are stored as uint8: n must be <= 256")
+    tx, ty = tiles
+    if x_dim % tx or y_dim % ty:
+        raise ValueError("tiles must divide the cube")
+    bx, by = x_dim // tx, y_dim // ty
+    basis = dct_basis(n)
+    m = measured_count(n)
+    P = x_dim * y_dim
+    coeffs = np.empty((P, n))
+    spectra = np.empty((P, n))
+    masks = np.empty((P, m), dtype=np.uint8)
+    y = np.empty((P, m))
+    seeds = []
+    # pixel (ix, iy) -> flat index ix * y_dim + iy (x-major, `solvers.py:497`)
+    flat = np.arange(P).reshape(x_dim, y_dim)
+    for i in range(tx):
+        for j in range(ty):
+            s = seed + ty * i + j
+            seeds.append(s)
+            c, f, mk, yy = _tile(bx * by, n, basis, s)
+            idx = flat[i * bx:(i + 1) * bx, j * by:(j + 1) * by].reshape(-1)
+            coeffs[idx], spectra[idx], masks[idx], y[idx] = c, f, mk, yy
+    return SyntheticCube(basis=basis, coeffs=coeffs, spectra=spectra, masks=masks, y=y,
+                         shape=(x_dim, y_dim), seeds=tuple(seeds))
+
+
+# BASELINE.json configs (shape, bands, tiling)
+CUBES = {
+    "jasper": dict(x_dim=100, y_dim=100, n=198),                 # cfg1, cfg2
+    "china": dict(x_dim=420, y_dim=140, n=154),                  # cfg3
+    "salinas": dict(x_dim=512, y_dim=217, n=224),                # cfg4
+    "scaling": dict(x_dim=2048, y_dim=868, n=224, tiles=(4, 4)),  # cfg5
+}
+
+
+def generate_named(name, seed=0):
+    spec = dict(CUBES[name])
+    return generate(seed=seed, **spec)

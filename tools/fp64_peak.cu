@@ -1,0 +1,127 @@
+// FP64 peak microbenchmark for B200 (sm_100a): DFMA (CUDA cores) and DMMA
+// (mma.sync f64 tensor path, m8n8k4 and m16n8k16).  Writes one JSON line.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  printf("{\"error\": \"%s line %d\"}\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+template <int ILP>
+__global__ void dfma_kernel(double* out, int iters, double a, double b) {
+  double acc[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) acc[i] = fma(acc[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s += acc[i];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int ILP>
+__global__ void dmma884_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[ILP][2];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { c[i][0] = i; c[i][1] = -i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int ILP>
+__global__ void dmma16816_kernel(double* out, int iters) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 1.0 - threadIdx.x * 1e-4 * i;
+  double c[ILP][4];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { c[i][0] = i; c[i][1] = -i; c[i][2] = 0; c[i][3] = 1; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <typename K>
+float time_kernel(K launch, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  launch();  // warm-up
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main() {
+  cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
+  int sms = prop.multiProcessorCount;
+  double* out; CK(cudaMalloc(&out, 1024 * sizeof(double)));
+  const int iters = 20000;
+  printf("{\"gpu\": \"%s\", \"sms\": %d", prop.name, sms);
+  for (int tpb : {256, 512, 1024}) {
+    int blocks = sms * (2048 / tpb);
+    float ms = time_kernel([&] { dfma_kernel<8><<<blocks, tpb>>>(out, iters, 0.999, 1e-3); }, 5);
+    double flops = 2.0 * 8 * iters * (double)blocks * tpb;
+    printf(", \"dfma_tflops_tpb%d\": %.2f", tpb, flops / ms / 1e9);
+  }
+  CK(cudaGetLastError());
+  for (int tpb : {128, 256, 512}) {
+    int blocks = sms * (1024 / tpb);
+    float ms = time_kernel([&] { dmma884_kernel<8><<<blocks, tpb>>>(out, iters); }, 5);
+    double flops = 2.0 * 8 * 8 * 4 * 8 * iters * (double)blocks * (tpb / 32);
+    printf(", \"dmma884_tflops_tpb%d\": %.2f", tpb, flops / ms / 1e9);
+  }
+  CK(cudaGetLastError());
+  for (int tpb : {128, 256, 512}) {
+    int blocks = sms * (1024 / tpb);
+    float ms = time_kernel([&] { dmma16816_kernel<4><<<blocks, tpb>>>(out, iters / 4); }, 5);
+    double flops = 2.0 * 16 * 8 * 16 * 4 * (iters / 4) * (double)blocks * (tpb / 32);
+    printf(", \"dmma16816_tflops_tpb%d\": %.2f", tpb, flops / ms / 1e9);
+  }
+  CK(cudaGetLastError());
+  // sustained: DMMA for ~4 s
+  {
+    int blocks = sms * 4, tpb = 256;
+    int it2 = 400000;
+    float ms = time_kernel([&] { dmma884_kernel<8><<<blocks, tpb>>>(out, it2); }, 2);
+    double flops = 2.0 * 8 * 8 * 4 * 8 * it2 * (double)blocks * (tpb / 32);
+    printf(", \"dmma884_sustained_tflops\": %.2f, \"sustained_ms\": %.1f", flops / ms / 1e9, ms);
+    ms = time_kernel([&] { dfma_kernel<8><<<blocks * 2, 512>>>(out, it2, 0.999, 1e-3); }, 2);
+    flops = 2.0 * 8 * it2 * (double)blocks * 2 * 512;
+    printf(", \"dfma_sustained_tflops\": %.2f", flops / ms / 1e9);
+  }
+  CK(cudaGetLastError());
+  printf("}\n");
+  return 0;
+}
