@@ -1,0 +1,135 @@
+/*
+ * hypercs_b200.h -- C ABI of the B200-native per-pixel compressive-sensing
+ * recovery library (libhypercs_b200.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path, the per-pixel
+ * solver API of `hypercs` (Python):
+ *
+ *   SOLVERS[name](y, dictionary, config) -> SolverResult
+ *       /root/reference/pkg/src/hypercs/solvers.py:164-403
+ *   recover_cube(measurements, dictionary, config, algorithm, jobs) -> (cube, RecoveryStats)
+ *       /root/reference/pkg/src/hypercs/solvers.py:455-514
+ *
+ * The reference has no FFI of its own (it is pure Python); its callers bind
+ * to the functions below through ctypes.  Conventions:
+ *
+ *   - every array pointer is a DEVICE pointer owned by the caller; arrays are
+ *     pixel-major and row-major (pixel p of an (x, y) cube is p = ix * Y + iy,
+ *     solvers.py:497);
+ *   - `basis` is the N x N orthonormal synthesis matrix Psi (f = Psi c) and
+ *     pixel p's dictionary is A_p = Psi[mask_p, :] (the reference's
+ *     Dictionary.matrix, transform.py:267-281, with one mask per pixel);
+ *   - N <= 256 (band indices are uint8), 1 <= M <= N, masks strictly increasing;
+ *   - all calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and reentrant; no global mutable state;
+ *   - return codes: HCS_OK, HCS_EINVAL (bad arguments: the Python layer raises
+ *     ValueError, same preconditions as the reference), HCS_ECUDA (CUDA error),
+ *     HCS_ENONFINITE (non-finite measurements where the reference raises
+ *     ValueError from scipy's finiteness check, solvers.py:227 /
+ *     kernels.py:61).  Per-pixel numerical failures never become error codes:
+ *     they go to stats.failed_at (solvers.py:445-452).
+ *     HCS_ENONFINITE is only known after the stream has executed, so it is
+ *     reported by hcs_recover_status(), not by hcs_recover().
+ */
+#ifndef HYPERCS_B200_H
+#define HYPERCS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCS_OK 0
+#define HCS_EINVAL 1
+#define HCS_ECUDA 2
+#define HCS_ENONFINITE 3
+
+/* algorithm ids, in the order of SOLVERS (solvers.py:397-403) */
+#define HCS_FISTA 0
+#define HCS_ADMM 1
+#define HCS_GOMP 2
+#define HCS_BIHT 3
+#define HCS_COSAMP 4
+
+#define HCS_MAX_N 256
+
+/* SolverConfig (solvers.py:40-85); max_iter <= 0 means no cap (None),
+ * time_limit <= 0 means no wall-clock budget (None).  The budget is per pixel,
+ * measured on the device from the moment the pixel is loaded (globaltimer),
+ * and checked before every iteration with the reference's precedence
+ * converged > timeout > cap (solvers.py:115-127). */
+typedef struct {
+  double lam;             /* l1 weight (fista, admm) */
+  double mu;              /* biht gradient step */
+  double alpha;           /* admm penalty rho */
+  double epsilon;         /* residual-delta convergence threshold */
+  int32_t kappa;          /* greedy target sparsity */
+  int32_t atoms_per_iter; /* gomp G; <= 0 -> max(1, kappa / 5) */
+  int32_t max_iter;       /* iteration cap; <= 0 -> unlimited */
+  int32_t reserved;
+  double time_limit;      /* seconds per pixel; <= 0 -> unlimited */
+} hcs_params;
+
+/* Per-pixel outputs (SolverResult fields, solvers.py:88-95).  Any pointer
+ * may be NULL except iterations/converged/final_delta/failed_at. */
+typedef struct {
+  int32_t* iterations;   /* P */
+  uint8_t* converged;    /* P */
+  double* final_delta;   /* P */
+  int32_t* failed_at;    /* P: -1 ok, else the NumericalFailure iteration */
+  double* admm_gap;      /* P: ||x - z|| (admm only; NaN for zero pixels) */
+  double* lipschitz;     /* P: power-iteration constant of A_p (fista) */
+  double* elapsed;       /* P: seconds the pixel spent in the solver (device clock) */
+  uint64_t* trace;       /* optional selection trace (greedy): P x trace_calls x 4 words,
+                            one 256-bit index bitmap per argmax_k call */
+  int32_t* trace_len;    /* P: number of argmax_k calls recorded */
+  int32_t trace_calls;   /* capacity per pixel */
+  int32_t reserved;
+} hcs_stats;
+
+/* Version of the ABI (major * 100 + minor). */
+int hcs_abi_version(void);
+
+/* Human-readable message for the last error on this host thread. */
+const char* hcs_last_error(void);
+
+/* Device workspace hcs_recover needs for (algo, P, N, M). */
+size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M);
+
+/* Recover P pixels with one algorithm: the body of recover_cube
+ * (solvers.py:455-514) for per-pixel dictionaries.  x_out is P x N. */
+int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis,
+                const double* y, const uint8_t* mask, const hcs_params* prm, double* x_out,
+                const hcs_stats* stats, void* workspace, size_t workspace_bytes, void* stream);
+
+/* After the stream has executed a hcs_recover call on `workspace`: HCS_OK or
+ * HCS_ENONFINITE (reads 4 bytes from the workspace; synchronises `stream`). */
+int hcs_recover_status(const void* workspace, void* stream);
+
+/* Batched kernels of hypercs.kernels (kernels.py:14-76). */
+int hcs_soft_threshold(int64_t n, const double* v, double t, double* out, void* stream);
+/* argmax_k (kernels.py:31-41) on P rows of length n: idx_out is P x k, ascending. */
+int hcs_argmax_k(int64_t P, int32_t n, const double* v, int32_t k, int32_t* idx_out, void* stream);
+/* least_squares (kernels.py:44-67) on P systems b_p (M x K row-major), y_p (M):
+ * s_out P x K; path_out (optional) P: 0 = pivoted-QR solve, 1 = minimum-norm fallback. */
+int hcs_least_squares(int64_t P, int32_t M, int32_t K, const double* b, const double* y,
+                      double* s_out, int32_t* path_out, void* stream);
+/* residual_delta (kernels.py:70-76) on P pairs of length n. */
+int hcs_residual_delta(int64_t P, int32_t n, const double* r, const double* r_prev, double* out,
+                       void* stream);
+/* lipschitz_constant (transform.py:176-217) of A_p = basis[mask_p, :]. */
+int hcs_lipschitz(int64_t P, int32_t N, int32_t M, const double* basis, const uint8_t* mask,
+                  double* out, void* stream);
+
+/* PSNR partial sums (metrics.py:30-55): sse_out[0] += sum (ref - basis @ x)^2
+ * over P x N, absmax_out[0] = max(absmax_out[0], max |ref|).  Accumulates, so
+ * the caller zeroes the two doubles once and may reduce them across ranks. */
+int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x,
+                      const double* basis, double* sse_out, double* absmax_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYPERCS_B200_H */

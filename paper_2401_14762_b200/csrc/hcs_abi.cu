@@ -1,0 +1,208 @@
+// hcs_abi.cu -- extern "C" entry points of libhypercs_b200.so (include/hypercs_b200.h).
+//
+// Host-side validation mirrors the reference's preconditions (solvers.py:67-85
+// config checks are done by the Python SolverConfig; the per-solver checks of
+// solvers.py:259-260, 306-307, 355-358 and the shape checks of :464-471 are
+// repeated here so a C caller gets HCS_EINVAL for the same inputs).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hypercs_b200.h"
+#include "hcs_gemm.cuh"
+#include "hcs_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(HCS_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr size_t kHeader = 256;   // counter (u64) + error flag (int)
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+inline int pad16(int n) { return (n + 15) & ~15; }
+
+int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+bool greedy(int algo) { return algo == HCS_GOMP || algo == HCS_BIHT || algo == HCS_COSAMP; }
+
+int greedy_ld(int M) { return (M + 1) | 1; }
+
+// LS matrices fit in shared memory up to this many bytes per CTA
+constexpr size_t kGreedySmemCap = 200 * 1024;
+
+}  // namespace
+
+extern "C" {
+
+int hcs_abi_version(void) { return 100; }
+
+const char* hcs_last_error(void) { return g_err.c_str(); }
+
+size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
+  (void)P;
+  size_t b = kHeader;
+  if (algo == HCS_FISTA || algo == HCS_ADMM) {
+    const int Np = pad16(N);
+    b += 2 * align256(sizeof(double) * (size_t)Np * Np);   // fragS, fragT
+    b += align256(sizeof(double) * (size_t)Np);            // u0
+  } else if (greedy(algo)) {
+    const int ld = greedy_ld(M);
+    const size_t ls = sizeof(double) * (size_t)M * ld;
+    if (hcs::greedy_smem_bytes(N, M, ld, false) > kGreedySmemCap)
+      b += align256(ls * (size_t)num_sms() * 4);
+  }
+  return b;
+}
+
+static int validate(int algo, int64_t P, int32_t N, int32_t M, const hcs_params* prm) {
+  if (algo < HCS_FISTA || algo > HCS_COSAMP) return fail(HCS_EINVAL, "unknown algorithm");
+  if (P < 0) return fail(HCS_EINVAL, "negative pixel count");
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (M < 1 || M > N) return fail(HCS_EINVAL, "M must be in [1, N]");
+  if (!prm) return fail(HCS_EINVAL, "null params");
+  if (prm->lam < 0) return fail(HCS_EINVAL, "lam must be >= 0");
+  if (prm->kappa < 1) return fail(HCS_EINVAL, "kappa must be >= 1");
+  if (prm->mu <= 0) return fail(HCS_EINVAL, "mu must be > 0");
+  if (prm->alpha <= 0) return fail(HCS_EINVAL, "alpha must be > 0");
+  if (prm->epsilon <= 0) return fail(HCS_EINVAL, "epsilon must be > 0");
+  const int G = prm->atoms_per_iter > 0 ? prm->atoms_per_iter : (prm->kappa / 5 > 1 ? prm->kappa / 5 : 1);
+  if (G < 1 || G > prm->kappa) return fail(HCS_EINVAL, "atoms_per_iter must be in [1, kappa]");
+  if (algo == HCS_GOMP && !(G <= prm->kappa && prm->kappa <= M))
+    return fail(HCS_EINVAL, "need atoms_per_iter <= kappa <= " + std::to_string(M));
+  if (algo == HCS_BIHT && prm->kappa > M) return fail(HCS_EINVAL, "kappa must be <= " + std::to_string(M));
+  if (algo == HCS_COSAMP) {
+    if (2 * prm->kappa > N) return fail(HCS_EINVAL, "need 2 * kappa <= " + std::to_string(N));
+    if (prm->kappa > M) return fail(HCS_EINVAL, "kappa must be <= " + std::to_string(M));
+  }
+  return HCS_OK;
+}
+
+int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, const double* y,
+                const uint8_t* mask, const hcs_params* prm, double* x_out, const hcs_stats* stats,
+                void* workspace, size_t workspace_bytes, void* stream_) {
+  int v = validate(algo, P, N, M, prm);
+  if (v != HCS_OK) return v;
+  if (!stats || !stats->iterations || !stats->converged || !stats->final_delta || !stats->failed_at)
+    return fail(HCS_EINVAL, "stats arrays iterations/converged/final_delta/failed_at are required");
+  if (workspace_bytes < hcs_workspace_bytes(algo, P, N, M)) return fail(HCS_EINVAL, "workspace too small");
+  if (P > 0 && (!basis || !y || !mask || !x_out || !workspace)) return fail(HCS_EINVAL, "null array");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  cudaError_t e = cudaMemsetAsync(ws, 0, kHeader, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  if (P == 0) return HCS_OK;
+
+  hcs::Stats st{stats->iterations, stats->converged, stats->final_delta, stats->failed_at, stats->admm_gap,
+                stats->lipschitz, stats->elapsed, stats->trace, stats->trace_len,
+                stats->trace ? stats->trace_calls : 0};
+  // the budget in whole nanoseconds, rounded down (elapsed >= limit, solvers.py:123)
+  const long long limit_ns = prm->time_limit > 0 ? (long long)(prm->time_limit * 1e9) : -1;
+  hcs::Params pr{prm->lam, prm->mu, prm->alpha, prm->epsilon, prm->kappa,
+                 prm->atoms_per_iter > 0 ? prm->atoms_per_iter : (prm->kappa / 5 > 1 ? prm->kappa / 5 : 1),
+                 prm->max_iter, algo, limit_ns};
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(ws);
+  int* err = reinterpret_cast<int*>(ws + 8);
+  const int sms = num_sms();
+
+  if (algo == HCS_FISTA || algo == HCS_ADMM) {
+    const int Np = pad16(N);
+    double2* fragS = reinterpret_cast<double2*>(ws + kHeader);
+    double2* fragT = reinterpret_cast<double2*>(ws + kHeader + align256(sizeof(double) * (size_t)Np * Np));
+    double* u0 = reinterpret_cast<double*>(ws + kHeader + 2 * align256(sizeof(double) * (size_t)Np * Np));
+    e = hcs::launch_prep_basis(basis, N, Np, fragS, fragT, u0, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "prep_basis_kernel");
+    hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, x_out, st, pr, counter, err};
+    const long long tiles = (P + hcs::kSlots - 1) / hcs::kSlots;
+    const int grid = (int)(tiles < sms ? tiles : sms);
+    e = hcs::launch_convex(algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm, args, grid, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "convex_kernel");
+    return HCS_OK;
+  }
+  const int ld = greedy_ld(M);
+  bool global_ls = hcs::greedy_smem_bytes(N, M, ld, false) > kGreedySmemCap;
+  const size_t smem = hcs::greedy_smem_bytes(N, M, ld, global_ls);
+  int per_sm = hcs::greedy_blocks_per_sm(algo, smem);
+  if (per_sm < 1) per_sm = 1;
+  if (global_ls && per_sm > 4) per_sm = 4;
+  long long grid = (long long)sms * per_sm;
+  if (grid > P) grid = P;
+  double* gscratch = global_ls ? reinterpret_cast<double*>(ws + kHeader) : nullptr;
+  hcs::GreedyArgs args{(long long)P, N, M, ld, basis, y, mask, x_out, st, pr, counter, err, gscratch};
+  e = hcs::launch_greedy(algo, args, (int)grid, smem, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "greedy_kernel");
+  return HCS_OK;
+}
+
+int hcs_recover_status(const void* workspace, void* stream_) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int flag = 0;
+  cudaError_t e = cudaMemcpyAsync(&flag, static_cast<const unsigned char*>(workspace) + 8, sizeof(int),
+                                  cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "status");
+  if (flag) return fail(HCS_ENONFINITE, "array must not contain infs or NaNs");
+  return HCS_OK;
+}
+
+int hcs_soft_threshold(int64_t n, const double* v, double t, double* out, void* stream) {
+  if (t < 0) return fail(HCS_EINVAL, "threshold must be >= 0");
+  if (n < 0) return fail(HCS_EINVAL, "negative length");
+  if (n == 0) return HCS_OK;
+  cudaError_t e = hcs::launch_soft(n, v, t, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "soft_threshold");
+}
+
+int hcs_argmax_k(int64_t P, int32_t n, const double* v, int32_t k, int32_t* idx_out, void* stream) {
+  if (n < 1 || n > HCS_MAX_N) return fail(HCS_EINVAL, "n must be in [1, 256]");
+  if (k < 1 || k > n) return fail(HCS_EINVAL, "k must be in [1, " + std::to_string(n) + "], got " + std::to_string(k));
+  if (P <= 0) return HCS_OK;
+  cudaError_t e = hcs::launch_argmax_k(P, n, v, k, idx_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "argmax_k");
+}
+
+int hcs_least_squares(int64_t P, int32_t M, int32_t K, const double* b, const double* y, double* s_out,
+                      int32_t* path_out, void* stream) {
+  if (M < 1 || K < 1 || M > HCS_MAX_N || K > HCS_MAX_N) return fail(HCS_EINVAL, "M and K must be in [1, 256]");
+  if (P <= 0) return HCS_OK;
+  cudaError_t e = hcs::launch_batched_ls(P, M, K, b, y, s_out, path_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "least_squares");
+}
+
+int hcs_residual_delta(int64_t P, int32_t n, const double* r, const double* r_prev, double* out, void* stream) {
+  if (n < 1) return fail(HCS_EINVAL, "n must be >= 1");
+  if (P <= 0) return HCS_OK;
+  cudaError_t e = hcs::launch_rdelta(P, n, r, r_prev, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "residual_delta");
+}
+
+int hcs_lipschitz(int64_t P, int32_t N, int32_t M, const double* basis, const uint8_t* mask, double* out,
+                  void* stream) {
+  if (N < 1 || N > HCS_MAX_N || M < 1 || M > N) return fail(HCS_EINVAL, "bad N/M");
+  if (P <= 0) return HCS_OK;
+  cudaError_t e = hcs::launch_lipschitz(P, N, M, basis, mask, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "lipschitz");
+}
+
+int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x, const double* basis, double* sse_out,
+                      double* absmax_out, void* stream) {
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (P <= 0) return HCS_OK;
+  cudaError_t e = hcs::launch_psnr(P, N, ref, x, basis, sse_out, absmax_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "psnr_partials");
+}
+
+}  // extern "C"

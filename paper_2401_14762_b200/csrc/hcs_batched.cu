@@ -1,0 +1,224 @@
+// hcs_batched.cu -- batched forms of the reference's numeric kernels
+// (hypercs/kernels.py:14-76), the Lipschitz constant (transform.py:176-217)
+// and the PSNR partial sums (metrics.py:30-55).  These back the kernel-level
+// parity tests and the output-side PSNR; the solvers use the same device
+// routines inline.
+#include "hcs_gemm.cuh"
+#include "hcs_internal.cuh"
+#include "hcs_ls.cuh"
+
+namespace hcs {
+
+__global__ void soft_kernel(long long n, const double* __restrict__ v, double t, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = soft(v[i], t);
+}
+
+cudaError_t launch_soft(long long n, const double* v, double t, double* out, cudaStream_t stream) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  soft_kernel<<<(int)blocks, 256, 0, stream>>>(n, v, t, out);
+  return cudaGetLastError();
+}
+
+// one warp per row
+__global__ void argmax_k_kernel(long long P, int n, const double* __restrict__ v, int k, int32_t* __restrict__ idx) {
+  __shared__ double row[4][kMaxN];
+  __shared__ uint32_t bm[4][8];
+  __shared__ int list[4][kMaxN];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long p = blockIdx.x * 4LL + w; p < P; p += (long long)gridDim.x * 4) {
+    for (int i = lane; i < n; i += 32) row[w][i] = v[p * n + i];
+    __syncwarp();
+    warp_topk(row[w], n, k, bm[w]);
+    const int cnt = [&] {
+      int base = 0;
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t word = bm[w][e];
+        if ((word >> lane) & 1u) list[w][base + __popc(word & ((1u << lane) - 1u))] = 32 * e + lane;
+        base += __popc(word);
+      }
+      return base;
+    }();
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) idx[p * k + i] = list[w][i];
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t* idx, cudaStream_t stream) {
+  long long blocks = (P + 3) / 4;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  argmax_k_kernel<<<(int)blocks, 128, 0, stream>>>(P, n, v, k, idx);
+  return cudaGetLastError();
+}
+
+// one CTA per system; b_p row-major M x K, y_p length M
+__global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, int ld, const double* __restrict__ b,
+                                                 const double* __restrict__ y, double* __restrict__ s,
+                                                 int32_t* __restrict__ path) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* B = reinterpret_cast<double*>(smraw);
+  double* sv = B + (size_t)M * ld;
+  double* vn1 = sv + K + 1;
+  double* vn2 = vn1 + K + 1;
+  double* zt = vn2 + K + 1;
+  double* red = zt + K + 1;
+  int* perm = reinterpret_cast<int*>(red + 16);
+  int* ipiv = perm + K + 1;
+  LsScratch sc{vn1, vn2, zt, perm, red, ipiv};
+  for (long long p = blockIdx.x; p < P; p += gridDim.x) {
+    for (int idx = threadIdx.x; idx < M * (K + 1); idx += blockDim.x) {
+      const int rr = idx / (K + 1), c = idx - rr * (K + 1);
+      B[rr * ld + c] = (c < K) ? b[(p * M + rr) * K + c] : y[p * M + rr];
+    }
+    __syncthreads();
+    const int pth = ls_solve(B, ld, M, K, sv, sc);
+    for (int c = threadIdx.x; c < K; c += blockDim.x) s[p * K + c] = sv[c];
+    if (path && threadIdx.x == 0) path[p] = pth;
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s, int32_t* path,
+                              cudaStream_t stream) {
+  const int ld = (K + 1) | 1;
+  const size_t smem = sizeof(double) * ((size_t)M * ld + 4 * (K + 1) + 16) + sizeof(int) * (K + 2);
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long long blocks = P < 148 * 4 ? P : 148 * 4;
+  ls_kernel<<<(int)blocks, 128, smem, stream>>>(P, M, K, ld, b, y, s, path);
+  return cudaGetLastError();
+}
+
+__global__ void rdelta_kernel(long long P, int n, const double* __restrict__ r, const double* __restrict__ rp,
+                              double* __restrict__ out) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long p = blockIdx.x * 4LL + w; p < P; p += (long long)gridDim.x * 4) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double d = r[p * n + i] - rp[p * n + i];
+      s += d * d;
+    }
+    s = warp_sum(s);
+    if (lane == 0) out[p] = sqrt(s);
+  }
+}
+
+cudaError_t launch_rdelta(long long P, int n, const double* r, const double* rp, double* out, cudaStream_t stream) {
+  long long blocks = (P + 3) / 4;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  rdelta_kernel<<<(int)blocks, 128, 0, stream>>>(P, n, r, rp, out);
+  return cudaGetLastError();
+}
+
+__global__ void lipschitz_kernel(long long P, int N, int M, const double* __restrict__ basis,
+                                 const uint8_t* __restrict__ mask, double* __restrict__ out) {
+  __shared__ double u0[kMaxN];
+  __shared__ uint8_t msk[4][kMaxN];
+  const double inv = 1.0 / sqrt((double)N);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < N; ++k) s += basis[(size_t)j * N + k] * inv;
+    u0[j] = s;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long p = blockIdx.x * 4LL + w; p < P; p += (long long)gridDim.x * 4) {
+    for (int j = lane; j < M; j += 32) msk[w][j] = mask[p * M + j];
+    __syncwarp();
+    const double L = warp_lipschitz(u0, msk[w], M);
+    if (lane == 0) out[p] = L;
+    __syncwarp();
+  }
+}
+
+cudaError_t launch_lipschitz(long long P, int N, int M, const double* basis, const uint8_t* mask, double* out,
+                             cudaStream_t stream) {
+  long long blocks = (P + 3) / 4;
+  if (blocks > 148 * 2) blocks = 148 * 2;
+  lipschitz_kernel<<<(int)blocks, 128, 0, stream>>>(P, N, M, basis, mask, out);
+  return cudaGetLastError();
+}
+
+// PSNR partials: tiles of 32 pixels, rec = Psi x by the DMMA tile GEMM with A
+// fragments read straight from the row-major basis (L1/L2 resident).
+__global__ void __launch_bounds__(512) psnr_kernel(long long P, int N, int Np, const double* __restrict__ ref,
+                                                   const double* __restrict__ x, const double* __restrict__ basis,
+                                                   double* sse, double* amax) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  double* In = reinterpret_cast<double*>(smraw);
+  __shared__ double red[32];
+  __shared__ double redm[32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  const int KS = Np >> 2;
+  double local = 0.0, lmax = 0.0;
+  for (long long t0 = blockIdx.x * (long long)kSlots; t0 < P; t0 += (long long)gridDim.x * kSlots) {
+    for (int idx = threadIdx.x; idx < Np * kSlots; idx += blockDim.x) {
+      const int s = idx / Np, n = idx - s * Np;
+      const long long p = t0 + s;
+      In[in_idx(n, s)] = (p < P && n < N) ? x[p * N + n] : 0.0;
+    }
+    __syncthreads();
+    double acc[2][4][2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks) {
+      const int c = 4 * ks + (lane & 3);
+      const int r0 = 16 * w + (lane >> 2), r1 = r0 + 8;
+      const double a0 = (r0 < N && c < N) ? __ldg(basis + (size_t)r0 * N + c) : 0.0;
+      const double a1 = (r1 < N && c < N) ? __ldg(basis + (size_t)r1 * N + c) : 0.0;
+      const double* b = In + (ks << 7) + lane;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        dmma(acc[0][cb], a0, b[32 * cb]);
+        dmma(acc[1][cb], a1, b[32 * cb]);
+      }
+    }
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int n = acc_row(w, rb, lane), s = acc_col(cb, i, lane);
+          const long long p = t0 + s;
+          if (p < P && n < N) {
+            const double f = ref[p * N + n];
+            const double d = f - acc[rb][cb][i];
+            local += d * d;
+            lmax = fmax(lmax, fabs(f));
+          }
+        }
+    __syncthreads();
+  }
+  local = warp_sum(local);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  if (lane == 0) { red[w] = local; redm[w] = lmax; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0, m = 0.0;
+    for (int i = 0; i < W; ++i) { s += red[i]; m = fmax(m, redm[i]); }
+    atomicAdd(sse, s);
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(amax), (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+cudaError_t launch_psnr(long long P, int N, const double* ref, const double* x, const double* basis, double* sse,
+                        double* amax, cudaStream_t stream) {
+  const int Np = (N + 15) & ~15;
+  const size_t smem = sizeof(double) * (size_t)Np * kSlots;
+  cudaError_t e = cudaFuncSetAttribute(psnr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long long tiles = (P + kSlots - 1) / kSlots;
+  int blocks = (int)(tiles < 148 * 2 ? tiles : 148 * 2);
+  psnr_kernel<<<blocks, 2 * Np, smem, stream>>>(P, N, Np, ref, x, basis, sse, amax);
+  return cudaGetLastError();
+}
+
+}  // namespace hcs

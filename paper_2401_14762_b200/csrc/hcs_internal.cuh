@@ -1,0 +1,59 @@
+// hcs_internal.cuh -- argument blocks and launchers shared by the translation
+// units of libhypercs_b200.so (not part of the public C ABI).
+#pragma once
+#include "hcs_common.cuh"
+
+namespace hcs {
+
+enum { kFista = 0, kAdmm = 1, kGomp = 2, kBiht = 3, kCosamp = 4 };
+
+struct ConvexArgs {
+  long long P;
+  int N, Np, M;
+  const double* y;
+  const uint8_t* mask;
+  const double2* fragT;   // Psi^T (analysis) in fragment order
+  const double2* fragS;   // Psi (synthesis) in fragment order
+  const double* u0;       // Psi * (1/sqrt(N)) 1, for the Lipschitz constant
+  double* x_out;
+  Stats st;
+  Params prm;
+  unsigned long long* counter;
+  int* err;
+};
+
+struct GreedyArgs {
+  long long P;
+  int N, M, ld;          // ld: row stride of the LS matrix (odd, >= M + 1)
+  const double* basis;   // Psi, N x N row-major
+  const double* y;
+  const uint8_t* mask;
+  double* x_out;
+  Stats st;
+  Params prm;
+  unsigned long long* counter;
+  int* err;
+  double* gscratch;      // non-null: LS matrices live in global memory (large M)
+};
+
+// hcs_convex.cu
+cudaError_t launch_convex(int algo, const ConvexArgs& args, int grid, cudaStream_t stream);
+size_t convex_smem_bytes(int algo, int Np, int M);
+cudaError_t launch_prep_basis(const double* basis, int N, int Np, double2* fragS, double2* fragT, double* u0,
+                              cudaStream_t stream);
+// hcs_greedy.cu
+cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream);
+size_t greedy_smem_bytes(int N, int M, int ld, bool global_ls);
+int greedy_blocks_per_sm(int algo, size_t smem);
+// hcs_batched.cu
+cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s,
+                              int32_t* path, cudaStream_t stream);
+cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t* idx, cudaStream_t stream);
+cudaError_t launch_soft(long long n, const double* v, double t, double* out, cudaStream_t stream);
+cudaError_t launch_rdelta(long long P, int n, const double* r, const double* rp, double* out, cudaStream_t stream);
+cudaError_t launch_lipschitz(long long P, int N, int M, const double* basis, const uint8_t* mask, double* out,
+                             cudaStream_t stream);
+cudaError_t launch_psnr(long long P, int N, const double* ref, const double* x, const double* basis, double* sse,
+                        double* amax, cudaStream_t stream);
+
+}  // namespace hcs
