@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark: recovered spectra/s per solver on the B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload scaling|cfg1..cfg4] [--impl ours|reference]
+
+Default workload = BASELINE config 5 (the scaling run the metric is quoted on:
+"1/2/4/8 B200"): a 2048 x 868 x 224 synthetic cube (4 x 4 tiles of the
+512 x 217 generator, seeds 0..15, 1,777,664 spectra, 90 measured bands per
+pixel) recovered by all ten solver configurations (FISTA/ADMM lambda in
+{0.1, 100}; gOMP/BIHT/CoSaMP kappa in {27, 33}, G = kappa // 5, mu = 0.1,
+eps = 1e-8, caps 5000/2000).  One step = recover the whole cube once with each
+configuration (+ PSNR partials + the stats all-reduce).  value = spectra
+recovered by all ranks per second (10 x P per step).  Pixel rows are sharded
+across ranks (strong scaling of a fixed cube); the only collective is one
+NCCL all-reduce of per-configuration PSNR/convergence sums per step.
+
+Inputs are generated on the host (paper_2401_14762_b200.synth v1) and are
+device-resident before timing; the per-step inputs (1.28 GB of measurements)
+exceed the 126 MB L2, so no flush is needed.  `--impl reference` times the
+CPU oracle (restatement of the reference's solvers; the reference is pure
+Python and is not installed on the GPU box) on a bounded pixel sample on all
+host cores, rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2401_14762_b200 import synth  # noqa: E402
+
+SCALING_SOLVERS = [
+    ("fista", dict(lam=0.1), 5000), ("fista", dict(lam=100.0), 5000),
+    ("admm", dict(lam=0.1, alpha=1.8), 5000), ("admm", dict(lam=100.0, alpha=1.8), 5000),
+    ("gomp", dict(kappa=27, atoms_per_iter=5), None), ("gomp", dict(kappa=33, atoms_per_iter=6), None),
+    ("biht", dict(kappa=27, mu=0.1), 2000), ("biht", dict(kappa=33, mu=0.1), 2000),
+    ("cosamp", dict(kappa=27), 2000), ("cosamp", dict(kappa=33), 2000),
+]
+WORKLOADS = {
+    "scaling": ("scaling", SCALING_SOLVERS),
+    "cfg1": ("jasper", [("gomp", dict(kappa=24, atoms_per_iter=4), None)]),
+    "cfg2": ("jasper", [("fista", dict(lam=100.0), 5000), ("admm", dict(lam=100.0, alpha=1.8), 5000)]),
+    "cfg3": ("china", [("biht", dict(kappa=22, mu=0.1), 2000), ("gomp", dict(kappa=22, atoms_per_iter=4), None)]),
+    "cfg4": ("salinas", [("cosamp", dict(kappa=33), 2000)]),
+}
+METRIC = "recovered spectra/sec (all solver configs of the workload)"
+
+
+def label(algo, params):
+    return algo + "_" + "_".join(f"{k[0] if k != 'atoms_per_iter' else 'G'}{v:g}" for k, v in params.items()
+                                  if k in ("lam", "kappa"))
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+
+
+def _oracle_rate(cube, solvers, budget_s, cores, seed=0, pool=None):
+    """Time the oracle on a bounded sample per solver config (one persistent
+    process pool over `cores` workers, OpenBLAS single-threaded per worker, as
+    BASELINE.md §2 prescribes).  Returns (spectra/s aggregated like the GPU
+    value, per-config rates, sample sizes)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from concurrent.futures import ProcessPoolExecutor
+    from oracle import cpu_solvers as oc
+    own = pool is None
+    if own:
+        pool = ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas)
+        list(pool.map(abs, range(4 * cores)))        # start the workers outside the timing
+    rng = np.random.default_rng(seed)
+    rates, sizes = {}, {}
+    P = cube.n_pixels
+    try:
+        for algo, params, cap in solvers:
+            cfg = oc.OracleConfig(max_iter=cap or 0, **params)
+            n = min(P, 4 * cores)
+            while True:
+                idx = np.sort(rng.choice(P, size=n, replace=False))
+                t0 = time.perf_counter()
+                oc.solve_cube(algo, cube.basis, cube.y[idx], cube.masks[idx], cfg,
+                              chunk=max(1, n // (4 * cores)), pool=pool)
+                dt = time.perf_counter() - t0
+                if dt >= 0.5 * budget_s or n >= P:
+                    break
+                n = int(min(P, max(2 * n, n * budget_s / max(dt, 1e-3))))
+            rates[label(algo, params)] = n / dt
+            sizes[label(algo, params)] = int(n)
+    finally:
+        if own:
+            pool.shutdown()
+    agg = len(solvers) / sum(1.0 / r for r in rates.values())
+    return agg, rates, sizes
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cube_name, solvers = WORKLOADS[args.workload]
+    spec = dict(synth.CUBES[cube_name])
+    # a bounded sample of the workload: the first tile (same generator, seed 0)
+    if "tiles" in spec:
+        tx, ty = spec.pop("tiles")
+        spec["x_dim"] //= tx
+        spec["y_dim"] //= ty
+    cube = synth.generate(seed=0, **spec)
+    cores = host_cores()
+    vals = []
+    from concurrent.futures import ProcessPoolExecutor
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle.cpu_solvers import single_thread_blas
+    with ProcessPoolExecutor(max_workers=cores, initializer=single_thread_blas) as pool:
+        list(pool.map(abs, range(4 * cores)))
+        for step in range(args.warmup + args.steps):
+            agg, rates, sizes = _oracle_rate(cube, solvers, args.ref_budget, cores, seed=step, pool=pool)
+            if step >= args.warmup:
+                vals.append((agg, rates, sizes))
+    value = float(np.mean([v[0] for v in vals]))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "spectra/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generator hcs-synth-v1)",
+        "config": {"workload": args.workload, "cube": cube_name, "solvers": [label(a, p) for a, p, _ in solvers]},
+        "per_solver": {k: float(np.mean([v[1][k] for v in vals])) for k in vals[0][1]},
+        "cpu_baseline": {"value": value, "unit": "spectra/s", "cores": cores, "kind": "port",
+                         "sample": f"per step and solver config ~{args.ref_budget:g}s of oracle work on random "
+                                   f"pixels of tile 0 of the workload cube ({cube.n_pixels} px), "
+                                   f"sizes {vals[-1][2]}"},
+        "e2e": {"value": value, "unit": "spectra/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"hcs_clocks_{os.getpid()}.csv"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={device_index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for row in self.path.read_text().splitlines():
+            parts = [p.strip() for p in row.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU leg
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2401_14762_b200 import _native
+    from paper_2401_14762_b200.metrics import psnr_partials
+    from paper_2401_14762_b200.solvers import SolverConfig, recover_cube, solve_batch
+    from paper_2401_14762_b200.transform import Dictionary
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.load()
+
+    cube_name, solvers = WORKLOADS[args.workload]
+    spec = synth.CUBES[cube_name]
+    X = spec["x_dim"]
+    x0, x1 = rank * X // world, (rank + 1) * X // world
+    t_gen = time.perf_counter()
+    cube = synth.generate_named(cube_name, x_range=(x0, x1), workers=min(16, host_cores()))
+    t_gen = time.perf_counter() - t_gen
+    P, n, m = cube.n_pixels, cube.n, cube.m
+    P_total = X * spec["y_dim"]
+
+    y_d = torch.as_tensor(cube.y, device=dev)
+    masks_d = torch.as_tensor(cube.masks, device=dev)
+    basis_d = torch.as_tensor(cube.basis, device=dev)
+    spectra_d = torch.as_tensor(cube.spectra, device=dev)
+    cfgs = [(a, p, SolverConfig(time_limit=None, max_iter=cap, **p)) for a, p, cap in solvers]
+    nsolv = len(cfgs)
+    stats_d = torch.zeros((nsolv, 5), dtype=torch.float64, device=dev)   # sse, conv, failed, zero, iters
+    psnr_d = torch.zeros((nsolv, 2), dtype=torch.float64, device=dev)    # sse, max|ref| (this rank)
+    # PSNR peak = max |reference spectra| over the whole cube: input-derived, reduced once at setup
+    peak_t = spectra_d.abs().max().reshape(1)
+    if world > 1:
+        dist.all_reduce(peak_t, op=dist.ReduceOp.MAX)
+    peak_ref = float(peak_t.item())
+    torch.cuda.synchronize()
+
+    out = None
+    launches_per_step = 0
+
+    def step(record=None):
+        nonlocal out, launches_per_step
+        launches = 0
+        psnr_d.zero_()
+        for i, (algo, params, cfg) in enumerate(cfgs):
+            if record is not None:
+                record[i][0].record()
+            b = solve_batch(algo, y_d, masks_d, basis_d, cfg, check_status=False, out=out)
+            if record is not None:
+                record[i][1].record()
+            out = b
+            psnr_partials(spectra_d, b.x, basis_d, out=psnr_d[i])
+            ok = b.failed_at < 0
+            stats_d[i, 1] = (b.converged.bool() & ok).sum()
+            stats_d[i, 2] = (~ok).sum()
+            stats_d[i, 3] = ((b.iterations == 0) & b.converged.bool() & ok).sum()
+            stats_d[i, 4] = b.iterations[ok].sum()
+            launches += b.launches + 1
+        stats_d[:, 0] = psnr_d[:, 0]
+        if world > 1:
+            dist.all_reduce(stats_d, op=dist.ReduceOp.SUM)   # the one data-path collective
+        launches_per_step = launches
+
+    # FP64 tensor peak of this GPU (roofline denominator)
+    peak_tf = _native.dmma_peak_tflops()
+
+    print(f"[bench] rank {rank}: {P} px generated in {t_gen:.1f}s; dmma peak {peak_tf:.1f} TF/s", file=sys.stderr,
+          flush=True)
+    for _ in range(args.warmup):
+        tw = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        print(f"[bench] warm-up step {time.perf_counter() - tw:.2f}s", file=sys.stderr, flush=True)
+    torch.cuda.synchronize()
+    if out is not None:
+        out.check_status()
+
+    ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in cfgs]
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(args.steps):
+        step(ev[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = t0.elapsed_time(t1) / 1e3
+    per_cfg = np.array([[ev[k][i][0].elapsed_time(ev[k][i][1]) / 1e3 for i in range(nsolv)]
+                        for k in range(args.steps)]).mean(axis=0)
+    tt = torch.tensor([elapsed, *per_cfg], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    elapsed = float(tt[0])
+    per_cfg = tt[1:].cpu().numpy()
+    stats = stats_d.cpu().numpy()
+
+    # roofline of the dominant kernel: the configuration with the longest launch
+    # (events around its hcs_recover call inside the timed region, max over ranks)
+    dom = int(np.argmax(per_cfg))
+    d_algo, d_params, _ = cfgs[dom]
+    convex = d_algo in ("fista", "admm")
+    flops_per_iter = 4.0 * n * n if convex else 2.0 * n * n
+    iters_all = float(stats[dom, 4])
+    achieved = flops_per_iter * iters_all / per_cfg[dom] / world / 1e12
+    roofline = {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved, "peak": peak_tf,
+                "frac": achieved / peak_tf, "traffic": None,
+                "kernel": ("convex_kernel<%s>" if convex else "greedy_kernel<%s>") % d_algo,
+                "config": label(d_algo, d_params), "launch_ms": 1e3 * per_cfg[dom],
+                "peak_source": "FP64 DMMA m8n8k4 throughput measured on this GPU by hcs_dmma_peak_tflops "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "algorithmic": (f"{flops_per_iter:.0f} FLOP per pixel-iteration "
+                                f"({'4' if convex else '2'} N^2, N={n}) x {iters_all:.0f} pixel-iterations "
+                                f"(all ranks) per launch; per GPU")}
+
+    total_spectra = P_total * nsolv * args.steps
+    value = total_spectra / elapsed
+    per_solver = {label(a, p): P_total / t for (a, p, _), t in zip(cfgs, per_cfg)}
+    quality = {}
+    for i, (a, p, _) in enumerate(cfgs):
+        sse, conv, failed, zero, iters = stats[i]
+        peak = peak_ref
+        mse = sse / (P_total * n)
+        quality[label(a, p)] = {"psnr_db": (math.inf if mse == 0 else 10 * math.log10(peak * peak / mse)),
+                                "convergence_pct": 100.0 * conv / P_total, "iterations": int(iters),
+                                "failed": int(failed)}
+
+    # ---- end to end through the public API, host (pinned) buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        y_h = torch.from_numpy(cube.y.reshape(x1 - x0, spec["y_dim"], m)).pin_memory()
+        dic = Dictionary.per_pixel(cube.basis, cube.masks)
+        h2d = d2h = 0
+        print(f"[bench] e2e warm-up", file=sys.stderr, flush=True)
+        for _ in range(1):   # warm-up of the e2e path
+            recover_cube(y_h, dic, cfgs[-1][2], cfgs[-1][0])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for k in range(args.e2e_steps):
+            for algo, _, cfg in cfgs:
+                dic._device = {}          # masks are re-uploaded every call
+                cube_h, st = recover_cube(y_h, dic, cfg, algo)
+                if k == 0:
+                    h2d += y_h.numel() * 8 + cube.masks.size
+                    d2h += cube_h.numel() * 8 + P * (4 + 1 + 8 + 4 + 8 + 8 + 8)
+        torch.cuda.synchronize()
+        te = time.perf_counter() - te
+        tte = torch.tensor([te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tte, op=dist.ReduceOp.MAX)
+        te = float(tte[0])
+        e2e = {"value": P_total * nsolv * args.e2e_steps / te, "unit": "spectra/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "paper_2401_14762_b200.recover_cube (pinned host measurements, per-pixel Dictionary)",
+               "steps": args.e2e_steps}
+
+    # ---- CPU baseline (rank 0, N = 1 only) --------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tile = synth.generate(spec["x_dim"] // spec.get("tiles", (1, 1))[0],
+                              spec["y_dim"] // spec.get("tiles", (1, 1))[1], n, seed=0)
+        cores = host_cores()
+        agg, rates, sizes = _oracle_rate(tile, solvers, args.cpu_budget, cores)
+        cpu = {"value": agg, "unit": "spectra/s", "cores": cores, "kind": "port",
+               "sample": f"~{args.cpu_budget:g}s of oracle work per solver config on random pixels of tile 0 "
+                         f"of the workload cube; sizes {sizes}",
+               "per_solver": rates}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "spectra/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generator hcs-synth-v1, host-generated, device-resident before timing)",
+            "config": {"workload": args.workload, "cube": cube_name, "shape": [X, spec["y_dim"], n],
+                       "pixels": P_total, "measured_bands": m, "solvers": [label(a, p) for a, p, _ in cfgs],
+                       "parallelism": f"pixel-row slabs x{world}", "l2": "inputs (1.28 GB/step) > 126 MB L2; no flush"},
+            "per_solver": per_solver, "quality": quality,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk, "generation_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="scaling", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=2.0, help="seconds of oracle work per solver config")
+    ap.add_argument("--ref-budget", type=float, default=0.3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -129,6 +129,11 @@ int hcs_lipschitz(int64_t P, int32_t N, int32_t M, const double* basis, const ui
 int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x,
                       const double* basis, double* sse_out, double* absmax_out, void* stream);
 
+/* FP64 tensor-core (DMMA m8n8k4) throughput of this GPU in TFLOP/s, best of 3
+ * launches of `iters` iterations on the legacy default stream: the roofline
+ * denominator for the FP64 GEMM phases (synchronises the device). */
+int hcs_dmma_peak_tflops(double* tflops_out, int iters);
+
 #ifdef __cplusplus
 }
 #endif

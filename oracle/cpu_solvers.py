@@ -393,6 +393,16 @@ class CubeResult:
     traces: list | None = None
 
 
+def single_thread_blas():
+    """Pool initializer: one BLAS thread per worker process."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
+
+
 def _solve_range(args):
     algo, basis, y, masks, cfg, want_trace = args
     out = []
@@ -403,9 +413,10 @@ def _solve_range(args):
     return out
 
 
-def solve_cube(algo, basis, y, masks, cfg, jobs=1, trace=False, chunk=64):
+def solve_cube(algo, basis, y, masks, cfg, jobs=1, trace=False, chunk=64, pool=None):
     """Per-pixel oracle over a (P, m) measurement array with per-pixel masks:
-    the reference's SOLVERS[algo] on Dictionary.from_matrix(Psi[mask_p])."""
+    the reference's SOLVERS[algo] on Dictionary.from_matrix(Psi[mask_p]).
+    ``pool``: an existing process pool to reuse (else one is made for jobs > 1)."""
     y = np.asarray(y, dtype=np.float64)
     masks = np.asarray(masks)
     P, m = y.shape
@@ -413,11 +424,12 @@ def solve_cube(algo, basis, y, masks, cfg, jobs=1, trace=False, chunk=64):
     check_preconditions(algo, m, n, cfg)
     items = [(algo, basis, y[i:i + chunk], masks[i:i + chunk], cfg, trace)
              for i in range(0, P, chunk)]
-    if jobs == 1 or P <= chunk:
+    if pool is not None:
+        parts = list(pool.map(_solve_range, items))
+    elif jobs == 1 or P <= chunk:
         parts = [_solve_range(it) for it in items]
     else:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        with ProcessPoolExecutor(max_workers=jobs) as pool:
+        with ProcessPoolExecutor(max_workers=jobs, initializer=single_thread_blas) as pool:
             parts = list(pool.map(_solve_range, items))
     flat = [r for part in parts for r in part]
     return CubeResult(

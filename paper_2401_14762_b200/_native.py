@@ -19,7 +19,7 @@ ALGO_IDS = {"fista": 0, "admm": 1, "gomp": 2, "biht": 3, "cosamp": 4}
 EXPORTS = (
     "hcs_abi_version", "hcs_last_error", "hcs_workspace_bytes", "hcs_recover", "hcs_recover_status",
     "hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta", "hcs_lipschitz",
-    "hcs_psnr_partials",
+    "hcs_psnr_partials", "hcs_dmma_peak_tflops",
 )
 
 
@@ -83,6 +83,8 @@ def load(path=None):
     lib.hcs_residual_delta.argtypes = [i64, i32, vp, vp, vp, vp]
     lib.hcs_lipschitz.argtypes = [i64, i32, i32, vp, vp, vp, vp]
     lib.hcs_psnr_partials.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp]
+    lib.hcs_dmma_peak_tflops.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    lib.hcs_dmma_peak_tflops.restype = ctypes.c_int
     for name in ("hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta",
                  "hcs_lipschitz", "hcs_psnr_partials"):
         getattr(lib, name).restype = ctypes.c_int
@@ -108,3 +110,11 @@ def stream_handle(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def dmma_peak_tflops(iters=20000):
+    """Measured FP64 DMMA peak of the current GPU (TFLOP/s)."""
+    out = ctypes.c_double(0.0)
+    if load().hcs_dmma_peak_tflops(ctypes.byref(out), iters) != 0:
+        raise RuntimeError("dmma peak microbenchmark failed")
+    return out.value

@@ -222,3 +222,54 @@ cudaError_t launch_psnr(long long P, int N, const double* ref, const double* x, 
 }
 
 }  // namespace hcs
+
+// ---------------------------------------------------------------------------
+// FP64 DMMA peak microbenchmark (the roofline denominator; MEASURED_PEAKS.json
+// carries no FP64 figure).  Independent m8n8k4 chains, 8 per warp.
+namespace hcs {
+__global__ void dmma_peak_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i][0] = i; c[i][1] = -i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+}  // namespace hcs
+
+extern "C" int hcs_dmma_peak_tflops(double* tflops_out, int iters) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* buf = nullptr;
+  if (cudaMalloc(&buf, 1024 * sizeof(double)) != cudaSuccess) return 2;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 4, threads = 256;
+  hcs::dmma_peak_kernel<<<blocks, threads>>>(buf, 1000);   // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    hcs::dmma_peak_kernel<<<blocks, threads>>>(buf, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * 8 * 8 * 4 * 8 * (double)iters * blocks * (threads / 32);
+  *tflops_out = flops / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}

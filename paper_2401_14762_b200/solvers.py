@@ -154,13 +154,23 @@ class DeviceBatch:
     elapsed: object      # (P,) float64
     trace: object = None
     trace_len: object = None
+    workspace: object = None
+    launches: int = 0        # kernels this call launched (prep + solver)
+
+    def check_status(self, stream=None):
+        """Raise ValueError where the reference raises on non-finite input (syncs)."""
+        nat.check(nat.load().hcs_recover_status(nat.ptr(self.workspace), nat.stream_handle(stream)))
 
 
-def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, workspace=None):
+def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, workspace=None,
+                check_status=True, out=None):
     """One hcs_recover call on device tensors: y (P, m) float64, masks (P, m)
     uint8, basis (n, n) float64, all CUDA.  Returns a DeviceBatch; raises
     ValueError exactly where the reference raises (config, preconditions,
-    non-finite measurements for admm/gomp/biht/cosamp)."""
+    non-finite measurements for admm/gomp/biht/cosamp).  With
+    check_status=False the call is fully asynchronous and the caller runs
+    ``batch.check_status()`` later.  ``out`` (a DeviceBatch of the same
+    algorithm and shape) reuses its buffers instead of allocating."""
     import torch
     if algorithm not in nat.ALGO_IDS:
         raise ValueError(f"unknown algorithm {algorithm!r}")
@@ -169,7 +179,11 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
     n = int(basis.shape[0])
     dev = y.device
     f64 = dict(dtype=torch.float64, device=dev)
-    out = DeviceBatch(
+    if out is not None and tuple(out.x.shape) == (P, n) and trace_calls == 0:
+        workspace = out.workspace if workspace is None else workspace
+    else:
+        out = None
+    out = out or DeviceBatch(
         x=torch.empty((P, n), **f64),
         iterations=torch.empty((P,), dtype=torch.int32, device=dev),
         converged=torch.empty((P,), dtype=torch.uint8, device=dev),
@@ -197,7 +211,10 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
     sh = nat.stream_handle(stream)
     nat.check(lib.hcs_recover(algo, P, n, m, nat.ptr(basis), nat.ptr(y), nat.ptr(masks), prm, nat.ptr(out.x),
                               st, nat.ptr(workspace), workspace.numel(), sh))
-    nat.check(lib.hcs_recover_status(nat.ptr(workspace), sh))
+    out.workspace = workspace
+    out.launches = (2 if algorithm in CONVEX_SOLVERS else 1) if P > 0 else 0
+    if check_status:
+        out.check_status(stream)
     return out
 
 
@@ -350,9 +367,13 @@ def recover_cube(measurements, dictionary, config, algorithm, jobs=1, stream=Non
     import torch
     if algorithm not in SOLVERS:
         raise ValueError(f"unknown algorithm {algorithm!r}")
-    on_device = isinstance(measurements, torch.Tensor) and measurements.is_cuda
-    if on_device:
-        meas = measurements.to(torch.float64)
+    is_torch = isinstance(measurements, torch.Tensor)
+    on_device = is_torch and measurements.is_cuda
+    host_torch = is_torch and not on_device       # e.g. a pinned host tensor
+    if is_torch:
+        if measurements.is_complex():
+            raise ValueError("the GPU backend is real-valued")
+        meas = measurements if measurements.dtype == torch.float64 else measurements.to(torch.float64)
     else:
         arr = np.asarray(measurements)
         if np.iscomplexobj(arr):
@@ -373,11 +394,21 @@ def recover_cube(measurements, dictionary, config, algorithm, jobs=1, stream=Non
     if algorithm == "admm":
         dictionary.admm_factor(config.alpha)
     t0 = time.perf_counter()
-    y_d = meas.reshape(P, m).contiguous() if on_device else torch.as_tensor(meas.reshape(P, m), device="cuda")
+    if on_device:
+        y_d = meas.reshape(P, m).contiguous()
+    elif host_torch:
+        y_d = meas.reshape(P, m).to("cuda", non_blocking=True)
+    else:
+        y_d = torch.as_tensor(meas.reshape(P, m), device="cuda")
     basis_d, masks_d = dictionary.device_arrays(y_d.device, P)
     b = solve_batch(algorithm, y_d, masks_d, basis_d, config, stream=stream)
     cube = b.x.reshape(x_dim, y_dim, dictionary.n)
-    if not on_device:
+    if host_torch:
+        host = torch.empty(cube.shape, dtype=torch.float64, pin_memory=True)
+        host.copy_(cube, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        cube = host
+    elif not on_device:
         cube = cube.cpu().numpy()
     wall = time.perf_counter() - t0
     x_flat = cube.reshape(P, dictionary.n)

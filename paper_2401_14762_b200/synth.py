@@ -126,37 +126,59 @@ def _tile(n_pix, n, basis, seed, chunk=1 << 16):
     return coeffs, spectra, masks, np.ascontiguousarray(y)
 
 
-def generate(x_dim, y_dim, n, seed=0, tiles=(1, 1)):
+def _tile_job(args):
+    n_pix, n, seed = args
+    return _tile(n_pix, n, dct_basis(n), seed)
+
+
+def generate(x_dim, y_dim, n, seed=0, tiles=(1, 1), x_range=None, workers=1):
     """Synthetic cube of shape (x_dim, y_dim, n), optionally tiled.
 
     With tiles=(tx, ty) the cube is made of tx*ty independent tiles of size
     (x_dim/tx, y_dim/ty), tile (i, j) seeded with seed + ty*i + j.
+    ``x_range=(x0, x1)`` returns only rows x0..x1-1 (a rank's slab; only the
+    tiles it touches are generated).  ``workers`` > 1 generates tiles in a
+    process pool (results are identical).
     """
     if n > 256:
         raise ValueError("band indices are stored as uint8: n must be <= 256")
     tx, ty = tiles
     if x_dim % tx or y_dim % ty:
         raise ValueError("tiles must divide the cube")
+    x0, x1 = x_range if x_range is not None else (0, x_dim)
+    if not 0 <= x0 <= x1 <= x_dim:
+        raise ValueError("bad x_range")
     bx, by = x_dim // tx, y_dim // ty
     basis = dct_basis(n)
     m = measured_count(n)
-    P = x_dim * y_dim
+    rows = x1 - x0
+    P = rows * y_dim
     coeffs = np.empty((P, n))
     spectra = np.empty((P, n))
     masks = np.empty((P, m), dtype=np.uint8)
     y = np.empty((P, m))
-    seeds = []
-    # pixel (ix, iy) -> flat index ix * y_dim + iy (x-major, `solvers.py:497`)
-    flat = np.arange(P).reshape(x_dim, y_dim)
+    jobs = []
     for i in range(tx):
+        lo, hi = max(x0, i * bx), min(x1, (i + 1) * bx)
+        if lo >= hi:
+            continue
         for j in range(ty):
-            s = seed + ty * i + j
-            seeds.append(s)
-            c, f, mk, yy = _tile(bx * by, n, basis, s)
-            idx = flat[i * bx:(i + 1) * bx, j * by:(j + 1) * by].reshape(-1)
-            coeffs[idx], spectra[idx], masks[idx], y[idx] = c, f, mk, yy
+            jobs.append((i, j, lo, hi))
+    specs = [(bx * by, n, seed + ty * i + j) for i, j, _, _ in jobs]
+    if workers > 1 and len(jobs) > 1:
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(max_workers=min(workers, len(jobs))) as pool:
+            parts = list(pool.map(_tile_job, specs))
+    else:
+        parts = [_tile(n_pix, n, basis, s) for n_pix, _, s in specs]
+    # pixel (ix, iy) -> flat index (ix - x0) * y_dim + iy (x-major, `solvers.py:497`)
+    flat = np.arange(P).reshape(rows, y_dim)
+    for (i, j, lo, hi), (c, f, mk, yy) in zip(jobs, parts):
+        keep = slice((lo - i * bx) * by, (hi - i * bx) * by)   # tile rows lo..hi-1, all columns
+        idx = flat[lo - x0:hi - x0, j * by:(j + 1) * by].reshape(-1)
+        coeffs[idx], spectra[idx], masks[idx], y[idx] = c[keep], f[keep], mk[keep], yy[keep]
     return SyntheticCube(basis=basis, coeffs=coeffs, spectra=spectra, masks=masks, y=y,
-                         shape=(x_dim, y_dim), seeds=tuple(seeds))
+                         shape=(rows, y_dim), seeds=tuple(s for _, _, s in specs))
 
 
 # BASELINE.json configs (shape, bands, tiling)
@@ -168,6 +190,6 @@ CUBES = {
 }
 
 
-def generate_named(name, seed=0):
+def generate_named(name, seed=0, x_range=None, workers=1):
     spec = dict(CUBES[name])
-    return generate(seed=seed, **spec)
+    return generate(seed=seed, x_range=x_range, workers=workers, **spec)
