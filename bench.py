@@ -215,6 +215,9 @@ def run_ours(args):
     _native.load()
 
     cube_name, solvers = WORKLOADS[args.workload]
+    if args.only:
+        keep = set(args.only.split(","))
+        solvers = [s for s in solvers if label(s[0], s[1]) in keep]
     spec = synth.CUBES[cube_name]
     X = spec["x_dim"]
     x0, x1 = rank * X // world, (rank + 1) * X // world
@@ -409,6 +412,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=0.3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--only", default="", help="comma-separated solver labels (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -39,10 +39,10 @@ int num_sms() {
 
 bool greedy(int algo) { return algo == HCS_GOMP || algo == HCS_BIHT || algo == HCS_COSAMP; }
 
-int greedy_ld(int M) { return (M + 1) | 1; }
 
 // LS matrices fit in shared memory up to this many bytes per CTA
 constexpr size_t kGreedySmemCap = 200 * 1024;
+constexpr int kMaxGreedyPerSm = 8;
 
 }  // namespace
 
@@ -60,10 +60,8 @@ size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
     b += 2 * align256(sizeof(double) * (size_t)Np * Np);   // fragS, fragT
     b += align256(sizeof(double) * (size_t)Np);            // u0
   } else if (greedy(algo)) {
-    const int ld = greedy_ld(M);
-    const size_t ls = sizeof(double) * (size_t)M * ld;
-    if (hcs::greedy_smem_bytes(N, M, ld, false) > kGreedySmemCap)
-      b += align256(ls * (size_t)num_sms() * 4);
+    // per-CTA global scratch for systems beyond the shared-memory region
+    b += align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm);
   }
   return b;
 }
@@ -132,16 +130,15 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     if (e != cudaSuccess) return cuda_fail(e, "convex_kernel");
     return HCS_OK;
   }
-  const int ld = greedy_ld(M);
-  bool global_ls = hcs::greedy_smem_bytes(N, M, ld, false) > kGreedySmemCap;
-  const size_t smem = hcs::greedy_smem_bytes(N, M, ld, global_ls);
-  int per_sm = hcs::greedy_blocks_per_sm(algo, smem);
+  const int kalloc = hcs::greedy_kalloc_host(algo, M, prm->kappa, kGreedySmemCap);
+  const size_t smem = hcs::greedy_smem_bytes(M, kalloc);
+  int per_sm = hcs::greedy_blocks_per_sm(algo, M, smem);
   if (per_sm < 1) per_sm = 1;
-  if (global_ls && per_sm > 4) per_sm = 4;
+  if (per_sm > kMaxGreedyPerSm) per_sm = kMaxGreedyPerSm;
   long long grid = (long long)sms * per_sm;
   if (grid > P) grid = P;
-  double* gscratch = global_ls ? reinterpret_cast<double*>(ws + kHeader) : nullptr;
-  hcs::GreedyArgs args{(long long)P, N, M, ld, basis, y, mask, x_out, st, pr, counter, err, gscratch};
+  double* gscratch = reinterpret_cast<double*>(ws + kHeader);
+  hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch};
   e = hcs::launch_greedy(algo, args, (int)grid, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "greedy_kernel");
   return HCS_OK;

@@ -6,8 +6,13 @@
 #include "hcs_gemm.cuh"
 #include "hcs_internal.cuh"
 #include "hcs_ls.cuh"
+#include "hcs_ls_blocked.cuh"
 
 namespace hcs {
+
+#ifdef HCS_PHASES
+__device__ unsigned long long g_phase_ls[16];
+#endif
 
 __global__ void soft_kernel(long long n, const double* __restrict__ v, double t, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -53,42 +58,93 @@ cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t*
   return cudaGetLastError();
 }
 
-// one CTA per system; b_p row-major M x K, y_p length M
-__global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, int ld, const double* __restrict__ b,
+// one CTA per system; b_p row-major M x K, y_p length M.  Blocked DMMA
+// Householder first (path 0), the exact pivoted restatement when its rank
+// guard trips (path 0 if that is full rank, 1 for the minimum-norm fallback).
+struct LsShared {
+  double red[16], Tm[64], G[64], tau[8], wsc[4 * 64];
+  int ipiv, flag;
+};
+
+__host__ __device__ inline size_t ls_batched_doubles(int M, int K) {
+  const int Mp = (M + 7) & ~7;
+  const size_t blk = (size_t)Mp * blocked_ld(K), piv = (size_t)M * ((K + 1) | 1);
+  return blk > piv ? blk : piv;
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, const double* __restrict__ b,
                                                  const double* __restrict__ y, double* __restrict__ s,
                                                  int32_t* __restrict__ path) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  const int Mp = (M + 7) & ~7;
   double* B = reinterpret_cast<double*>(smraw);
-  double* sv = B + (size_t)M * ld;
+  double* yv = B + ls_batched_doubles(M, K);
+  double* sv = yv + Mp;
   double* vn1 = sv + K + 1;
   double* vn2 = vn1 + K + 1;
   double* zt = vn2 + K + 1;
-  double* red = zt + K + 1;
-  int* perm = reinterpret_cast<int*>(red + 16);
-  int* ipiv = perm + K + 1;
-  LsScratch sc{vn1, vn2, zt, perm, red, ipiv};
+  LsShared* sh = reinterpret_cast<LsShared*>(zt + K + 1);
+  int* perm = reinterpret_cast<int*>(sh + 1);
+  const LsScratch sc{vn1, vn2, zt, perm, sh->red, &sh->ipiv};
+  const BlockedScratch bs{yv, sh->Tm, sh->G, sh->wsc, sh->tau, zt, &sh->flag};
+  const int ldb = blocked_ld(K), Kp = (K + 7) & ~7, ldp = (K + 1) | 1;
+#ifdef HCS_PHASES
+  long long hcs_ph[16] = {0};
+  hcs_ph[15] = clock64();
+  long long* php = hcs_ph;
+#else
+  long long* php = nullptr;
+#endif
   for (long long p = blockIdx.x; p < P; p += gridDim.x) {
-    for (int idx = threadIdx.x; idx < M * (K + 1); idx += blockDim.x) {
-      const int rr = idx / (K + 1), c = idx - rr * (K + 1);
-      B[rr * ld + c] = (c < K) ? b[(p * M + rr) * K + c] : y[p * M + rr];
+    int pth = 0;
+    bool done = false;
+    if (M >= K) {
+      for (int idx = threadIdx.x; idx < Mp * Kp; idx += blockDim.x) {
+        const int rr = idx / Kp, c = idx - rr * Kp;
+        B[rr * ldb + c] = (rr < M && c < K) ? b[(p * M + rr) * K + c] : 0.0;
+      }
+      for (int rr = threadIdx.x; rr < Mp; rr += blockDim.x) yv[rr] = rr < M ? y[p * M + rr] : 0.0;
+      __syncthreads();
+      HCS_MARKP(php, 3);
+      done = ls_blocked<NQ>(B, ldb, M, K, sv, bs, php);
     }
-    __syncthreads();
-    const int pth = ls_solve(B, ld, M, K, sv, sc);
+    if (!done) {
+      for (int idx = threadIdx.x; idx < M * (K + 1); idx += blockDim.x) {
+        const int rr = idx / (K + 1), c = idx - rr * (K + 1);
+        B[rr * ldp + c] = (c < K) ? b[(p * M + rr) * K + c] : y[p * M + rr];
+      }
+      __syncthreads();
+      pth = ls_solve(B, ldp, M, K, sv, sc);
+    }
     for (int c = threadIdx.x; c < K; c += blockDim.x) s[p * K + c] = sv[c];
     if (path && threadIdx.x == 0) path[p] = pth;
     __syncthreads();
+    HCS_MARKP(php, 10);
   }
+#ifdef HCS_PHASES
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 15; ++k) atomicAdd(&g_phase_ls[k], (unsigned long long)hcs_ph[k]);
+#endif
 }
 
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s, int32_t* path,
                               cudaStream_t stream) {
-  const int ld = (K + 1) | 1;
-  const size_t smem = sizeof(double) * ((size_t)M * ld + 4 * (K + 1) + 16) + sizeof(int) * (K + 2);
+  const int Mp = (M + 7) & ~7;
+  const size_t smem = sizeof(double) * (ls_batched_doubles(M, K) + Mp + 4 * (K + 1)) + sizeof(LsShared) +
+                      sizeof(int) * (K + 2);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   long long blocks = P < 148 * 4 ? P : 148 * 4;
-  ls_kernel<<<(int)blocks, 128, smem, stream>>>(P, M, K, ld, b, y, s, path);
+  cudaError_t e;
+  if (Mp <= 96) {
+    e = cudaFuncSetAttribute(ls_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ls_kernel<3><<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
+  } else {
+    e = cudaFuncSetAttribute(ls_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ls_kernel<8><<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
+  }
   return cudaGetLastError();
 }
 
@@ -272,4 +328,20 @@ extern "C" int hcs_dmma_peak_tflops(double* tflops_out, int iters) {
   cudaEventDestroy(e1);
   cudaFree(buf);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+// debug builds: per-phase cycle totals of the batched least-squares kernel
+extern "C" int hcs_debug_phases_ls(unsigned long long* out16, int reset) {
+#ifdef HCS_PHASES
+  cudaMemcpyFromSymbol(out16, hcs::g_phase_ls, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(hcs::g_phase_ls, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return 1;
+#endif
 }

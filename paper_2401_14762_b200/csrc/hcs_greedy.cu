@@ -3,41 +3,106 @@
 // Reference: hypercs/solvers.py:248-297 (gomp), :300-342 (biht), :345-394
 // (cosamp), stop rule :115-127, y = 0 shortcut :145-152, non-finite failure
 // :155-157; selection = kernels.argmax_k (kernels.py:31-41), least squares =
-// kernels.least_squares (kernels.py:44-67) -> hcs_ls.cuh.
+// kernels.least_squares (kernels.py:44-67).
 //
-// Each CTA (128 threads) pulls pixels from a global atomic work queue and runs
-// the whole solver for that pixel out of shared memory:
+// Each CTA (4 warps) pulls pixels from a global atomic work queue and runs the
+// whole solver for that pixel out of shared memory:
 //   * correlation p = A^T r = sum_j r_j Psi[mask_j, :]  (threads over bands,
 //     Psi rows streamed from L2; 2NM flops);
 //   * warp top-k by MSB-first key bisection (exact tie rule of argmax_k);
 //   * support sets as 256-bit bitmaps; union = OR, sorted list = ballot/popc;
 //   * the support-outgrew-m break happens before the solve and without
 //     counting the iteration (solvers.py:274-276, 320-321, 372-373);
-//   * column-pivoted Householder least squares on the gathered M x k
-//     dictionary columns (+ rhs) in shared memory;
+//   * least squares on the gathered M x k dictionary columns: blocked
+//     Householder on DMMA tensor cores (hcs_ls_blocked.cuh), falling back to
+//     the exact column-pivoted restatement (hcs_ls.cuh) when the rank guard
+//     trips;
 //   * residual y - A x recomputed from Psi rows, delta and the stop rule.
 // Optional trace: the 256-bit bitmap of every argmax_k call, for the parity
 // harness's tie classification.
-#include "hcs_ls.cuh"
 #include "hcs_internal.cuh"
+#include "hcs_ls.cuh"
+#include "hcs_ls_blocked.cuh"
 
 namespace hcs {
 
+#ifdef HCS_PHASES
+__device__ unsigned long long g_phase[16];
+#endif
+
 constexpr int kGreedyThreads = 128;
+constexpr int kRing = 8;   // states kept for cycle detection (periods 2..7)
 
 struct GreedyShared {
   uint32_t supp[8], sel[8], keep[8];
   double red[16];
+  double Tm[128], G[64], tau[16];
+  double wsc[4 * 64];
+  uint32_t ringbm[kRing][8];
   long long pid;
   long long start;
+  int mis;
+  int period;
   int dec;
   int ipiv;
   int count;
   int brk;
-  int bad;
+  int flag;
 };
 
-// Sorted index list of a 256-bit bitmap (warp 0); returns the count.
+// Shared-memory layout (doubles unless noted), identical on host and device.
+// The LS matrix region holds systems of up to `kalloc` columns; larger
+// systems (rare: gOMP supports beyond kalloc) use the CTA's global scratch.
+struct GreedyLayout {
+  int Mp, bmax;              // padded rows; doubles reserved for the LS matrix
+  int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring;   // double offsets
+  int ints;                  // int region offset (in doubles)
+  size_t bytes;
+};
+
+__host__ __device__ inline int ls_doubles(int M, int K) {
+  const int Mp = (M + 7) & ~7;
+  const int piv = M * ((K + 1) | 1);
+  const int blk = Mp * blocked_ld(K);
+  return piv > blk ? piv : blk;
+}
+
+__host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
+  GreedyLayout L;
+  L.Mp = (M + 7) & ~7;
+  L.bmax = ls_doubles(M, kalloc);
+  int o = L.bmax;
+  L.vec = o; o += kMaxN;
+  L.x = o; o += kMaxN;
+  L.ys = o; o += M;
+  L.r = o; o += M;
+  L.yv = o; o += L.Mp;
+  L.sv = o; o += M + 2;
+  L.vn1 = o; o += M + 2;
+  L.vn2 = o; o += M + 2;
+  L.zt = o; o += M + 2;
+  L.keys = o; o += kMaxN;
+  L.ring = o; o += kRing * M;
+  L.ints = o;
+  // ints: perm (M + 2), list (256), tlist (256); then msk bytes, then GreedyShared
+  size_t b = sizeof(double) * (size_t)o + sizeof(int) * (size_t)(M + 2 + 2 * kMaxN) + (size_t)M;
+  b = (b + 15) & ~(size_t)15;
+  b += sizeof(GreedyShared);
+  L.bytes = (b + 15) & ~(size_t)15;
+  return L;
+}
+
+// Columns the shared-memory LS region is sized for: the largest system each
+// solver builds on its fast path (support bounds of solvers.py:273, 319, 371).
+__host__ __device__ inline int greedy_kalloc(int algo, int M, int kappa) {
+  int k = M;
+  if (algo == kCosamp) k = 3 * kappa;           // kept kappa + 2 kappa new
+  else if (algo == kBiht) k = 2 * kappa;        // supp(x) <= kappa + kappa new
+  else if (algo == kGomp) k = kappa > 40 ? kappa : 40;   // refit kappa; supports beyond 40 spill
+  return k < M ? k : M;
+}
+
+// Sorted index list of a 256-bit bitmap (one warp); returns the count.
 __device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, int* list) {
   const int lane = threadIdx.x & 31;
   int base = 0;
@@ -52,30 +117,67 @@ __device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, int* list) {
   return base;
 }
 
-template <int ALGO>
-__global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
+template <int ALGO, int NQ>
+__global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int N = a.N, M = a.M, ld = a.ld;
+  const int N = a.N, M = a.M;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int KMAX = M + 1;  // support <= m (break before solve) ... +1 guard
-  // ---- shared memory carve-up -------------------------------------------
-  double* Bs = reinterpret_cast<double*>(smraw);
-  double* B = a.gscratch ? a.gscratch + (size_t)blockIdx.x * M * ld : Bs;
-  double* vec = Bs + (a.gscratch ? 0 : (size_t)M * ld);   // N: p / u / x_full
-  double* x = vec + kMaxN;                                 // N: current iterate
-  double* ys = x + kMaxN;                                  // M
-  double* r = ys + M;                                      // M
-  double* sv = r + M;                                      // KMAX: LS solution
-  double* vn1 = sv + KMAX + 1;
-  double* vn2 = vn1 + KMAX + 1;
-  double* zt = vn2 + KMAX + 1;
-  int* perm = reinterpret_cast<int*>(zt + KMAX + 1);       // KMAX + 1
-  int* list = perm + KMAX + 1;                             // 256: sorted support
-  int* tlist = list + kMaxN;                               // 256: refit support (gomp top)
-  uint8_t* msk = reinterpret_cast<uint8_t*>(tlist + kMaxN);  // M
+  const int kalloc = a.kalloc;
+  const GreedyLayout L = greedy_layout(M, kalloc);
+  double* S = reinterpret_cast<double*>(smraw);
+  double* Bglob = a.gscratch + (size_t)blockIdx.x * ls_doubles(M, M);
+  double* vec = S + L.vec;      // N: p / u / x_full
+  double* x = S + L.x;          // N: current iterate
+  double* ys = S + L.ys;        // M
+  double* r = S + L.r;          // M
+  double* yv = S + L.yv;        // Mp: blocked rhs
+  double* sv = S + L.sv;        // LS solution
+  int* perm = reinterpret_cast<int*>(S + L.ints);
+  int* list = perm + M + 2;     // sorted support
+  int* tlist = list + kMaxN;    // support of the new iterate
+  uint8_t* msk = reinterpret_cast<uint8_t*>(tlist + kMaxN);
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(S + L.keys);
+  double* ring = S + L.ring;    // kRing residuals (cycle detection)
   GreedyShared& g = *reinterpret_cast<GreedyShared*>(reinterpret_cast<uintptr_t>(msk + M + 15) & ~uintptr_t(15));
-  LsScratch sc{vn1, vn2, zt, perm, g.red, &g.ipiv};
+  const LsScratch sc{S + L.vn1, S + L.vn2, S + L.zt, perm, g.red, &g.ipiv};
+  const BlockedScratch bs{yv, g.Tm, g.G, g.wsc, g.tau, S + L.zt, &g.flag};
   const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+  const int Mp = L.Mp;
+#ifdef HCS_PHASES
+  long long hcs_ph[16] = {0};
+  hcs_ph[15] = clock64();
+  long long* php = hcs_ph;
+#define GMARK(k) HCS_MARKP(php, k)
+#else
+  long long* php = nullptr;
+#define GMARK(k) do {} while (0)
+#endif
+
+  // least squares on the dictionary columns `cols[0..K)` (+ y): blocked DMMA
+  // Householder, exact pivoted restatement when the rank guard trips
+  auto solve = [&](const int* cols, int K) {
+    double* B = K <= kalloc ? S : Bglob;
+    const int ldb = blocked_ld(K);
+    const int Kp = (K + 7) & ~7;
+    // warp w gathers rows w, w+4, ...; lanes over columns (coalesced within a Psi row)
+    for (int rr = warp; rr < Mp; rr += 4) {
+      const double* row = a.basis + (size_t)(rr < M ? msk[rr] : 0) * N;
+      for (int c = lane; c < Kp; c += 32)
+        B[rr * ldb + c] = (rr < M && c < K) ? __ldg(row + cols[c]) : 0.0;
+    }
+    for (int rr = tid; rr < Mp; rr += nt) yv[rr] = rr < M ? ys[rr] : 0.0;
+    __syncthreads();
+    GMARK(3);
+    if (ls_blocked<NQ>(B, ldb, M, K, sv, bs, php)) return;
+    const int ldp = (K + 1) | 1;
+    for (int idx = tid; idx < M * (K + 1); idx += nt) {
+      const int rr = idx / (K + 1), c = idx - rr * (K + 1);
+      B[rr * ldp + c] = (c < K) ? __ldg(a.basis + (size_t)msk[rr] * N + cols[c]) : ys[rr];
+    }
+    __syncthreads();
+    ls_solve(B, ldp, M, K, sv, sc);
+    GMARK(9);
+  };
 
   for (;;) {
     if (tid == 0) g.pid = (long long)atomicAdd(a.counter, 1ull);
@@ -93,15 +195,17 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
       bad |= !isfinite(v);
     }
     for (int n = tid; n < kMaxN; n += nt) x[n] = 0.0;
-    if (tid < 8) { g.supp[tid] = 0u; }
+    if (tid < 8) g.supp[tid] = 0u;
+    if (tid == 0) g.start = now_ns();
     nz = __syncthreads_or(nz);
     bad = __syncthreads_or(bad);
-    if (!nz) {   // y == 0 shortcut
+    if (!nz || bad) {   // y == 0 shortcut; non-finite y: scipy raises ValueError (kernels.py:61)
+      if (bad && tid == 0) atomicOr(a.err, 1);
       for (int n = tid; n < N; n += nt) a.x_out[pid * N + n] = 0.0;
       if (tid == 0) {
         a.st.iterations[pid] = 0;
-        a.st.converged[pid] = 1;
-        a.st.final_delta[pid] = 0.0;
+        a.st.converged[pid] = bad ? 0 : 1;
+        a.st.final_delta[pid] = bad ? NaN : 0.0;
         a.st.failed_at[pid] = -1;
         if (a.st.trace_len) a.st.trace_len[pid] = 0;
         if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
@@ -109,46 +213,46 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
       __syncthreads();
       continue;
     }
-    if (bad) {   // scipy's finiteness check raises ValueError (kernels.py:61)
-      if (tid == 0) atomicOr(a.err, 1);
-      for (int n = tid; n < N; n += nt) a.x_out[pid * N + n] = 0.0;
-      if (tid == 0) {
-        a.st.iterations[pid] = 0;
-        a.st.converged[pid] = 0;
-        a.st.final_delta[pid] = NaN;
-        a.st.failed_at[pid] = -1;
-        if (a.st.trace_len) a.st.trace_len[pid] = 0;
-        if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
-      }
-      __syncthreads();
-      continue;
-    }
+    const long long t0 = g.start;
     double delta = 1.0;
     int iters = 0, ncall = 0, ksupp = 0;
     bool converged = false, failed = false;
-    if (tid == 0) g.start = now_ns();
-    __syncthreads();
-    const long long t0 = g.start;
+    // Cycle skip (CoSaMP / gOMP): the next pass is a deterministic function of
+    // (support, residual) and y, so once that state recurs bit for bit after p
+    // passes the trajectory is exactly p-periodic; whole periods up to the cap
+    // are skipped, giving the same x, delta and iteration count as iterating.
+    // Disabled under a wall-clock budget (timeouts depend on elapsed time).
+    bool skipped = !(ALGO != kBiht && a.prm.limit_ns < 0 && a.prm.max_iter > 0);
     for (;;) {
       // ---- stop rule before the pass (solvers.py:115-127) -------------------
       if (tid == 0) g.dec = stop_decision(delta, iters, t0, a.prm);
       __syncthreads();
       const int dec = g.dec;
-      __syncthreads();
+      GMARK(0);
       if (dec != kContinue) { converged = dec == kConverged; break; }
       // ---- correlation / gradient proxy over all bands ----------------------
       for (int n = tid; n < N; n += nt) {
-        double p = 0.0;
-        for (int j = 0; j < M; ++j) p += r[j] * __ldg(a.basis + (size_t)msk[j] * N + n);
+        double p0 = 0.0, p1 = 0.0;
+        int j = 0;
+#pragma unroll 4
+        for (; j + 1 < M; j += 2) {
+          p0 += r[j] * __ldg(a.basis + (size_t)msk[j] * N + n);
+          p1 += r[j + 1] * __ldg(a.basis + (size_t)msk[j + 1] * N + n);
+        }
+        if (j < M) p0 += r[j] * __ldg(a.basis + (size_t)msk[j] * N + n);
+        double p = p0 + p1;
         if (ALGO == kBiht) p = __dadd_rn(x[n], __dmul_rn(a.prm.mu, p));   // solvers.py:318
         vec[n] = p;
       }
       __syncthreads();
+      GMARK(1);
       // ---- selection + union ------------------------------------------------
-      if (warp == 0) {
+      {
         const int k = (ALGO == kGomp) ? a.prm.G : (ALGO == kBiht ? a.prm.kappa : 2 * a.prm.kappa);
-        warp_topk(vec, N, k, g.sel);
+        cta_topk(vec, N, k, g.sel, keys);
         trace_store(a.st, pid, ncall, g.sel);
+      }
+      if (warp == 0) {
         if (lane < 8) {
           uint32_t u = g.sel[lane];
           if (ALGO == kBiht) {   // union with flatnonzero(x)
@@ -165,57 +269,45 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
         if (lane == 0) { g.count = cnt; g.brk = cnt > M; }
       }
       __syncthreads();
+      GMARK(2);
       if (g.brk) break;                          // keep the last iterate, no count
       ksupp = g.count;
-      // ---- gather A[:, support] and y, least squares --------------------------
-      for (int idx = tid; idx < M * (ksupp + 1); idx += nt) {
-        const int rr = idx / (ksupp + 1), c = idx - rr * (ksupp + 1);
-        B[rr * ld + c] = (c < ksupp) ? __ldg(a.basis + (size_t)msk[rr] * N + list[c]) : ys[rr];
-      }
-      __syncthreads();
-      ls_solve(B, ld, M, ksupp, sv, sc);
-      int kx;          // support size of the new iterate, indices in tlist
+      solve(list, ksupp);
+      int kx;          // support size of the new iterate, indices in tlist, values in sv
       if (ALGO == kGomp) {
         // x = scatter(s); top = argmax_k(x, kappa) over all N; refit on top
         for (int n = tid; n < N; n += nt) vec[n] = 0.0;
         __syncthreads();
         for (int c = tid; c < ksupp; c += nt) vec[list[c]] = sv[c];
         __syncthreads();
-        if (warp == 0) {
-          warp_topk(vec, N, a.prm.kappa, g.sel);
-          trace_store(a.st, pid, ncall, g.sel);
-          bitmap_to_list(g.sel, tlist);
-        }
+        cta_topk(vec, N, a.prm.kappa, g.sel, keys);
+        trace_store(a.st, pid, ncall, g.sel);
+        if (warp == 0) bitmap_to_list(g.sel, tlist);
         __syncthreads();
         kx = a.prm.kappa;
-        for (int idx = tid; idx < M * (kx + 1); idx += nt) {
-          const int rr = idx / (kx + 1), c = idx - rr * (kx + 1);
-          B[rr * ld + c] = (c < kx) ? __ldg(a.basis + (size_t)msk[rr] * N + tlist[c]) : ys[rr];
-        }
-        __syncthreads();
-        ls_solve(B, ld, M, kx, sv, sc);
+        solve(tlist, kx);
       } else {
         // keep = argmax_k(s, min(kappa, k)); zero (biht) or drop (cosamp) the rest
         const int kk = a.prm.kappa < ksupp ? a.prm.kappa : ksupp;
-        if (warp == 0) {
-          warp_topk(sv, ksupp, kk, g.keep);
-          trace_store(a.st, pid, ncall, g.keep);
-          if (ALGO == kCosamp) {
-            // support = support[keep]  (stays sorted)
-            if (lane == 0) {
-              int o = 0;
-              for (int c = 0; c < ksupp; ++c)
-                if (bm_test(g.keep, c)) { tlist[o] = list[c]; zt[o] = sv[c]; ++o; }
-              for (int e = 0; e < 8; ++e) g.supp[e] = 0u;
-              for (int c = 0; c < o; ++c) g.supp[tlist[c] >> 5] |= 1u << (tlist[c] & 31);
+        double* zt = S + L.zt;
+        cta_topk(sv, ksupp, kk, g.keep, keys);
+        trace_store(a.st, pid, ncall, g.keep);
+        if (ALGO == kCosamp) {   // support = support[keep]  (stays sorted)
+          if (tid < 8) g.supp[tid] = 0u;
+          __syncthreads();
+          for (int c = tid; c < ksupp; c += nt) {
+            if (bm_test(g.keep, c)) {
+              int o = __popc(g.keep[c >> 5] & ((1u << (c & 31)) - 1u));
+              for (int e = 0; e < (c >> 5); ++e) o += __popc(g.keep[e]);
+              tlist[o] = list[c];
+              zt[o] = sv[c];
+              atomicOr(&g.supp[list[c] >> 5], 1u << (list[c] & 31));
             }
-          } else {
-            if (lane == 0) {
-              for (int c = 0; c < ksupp; ++c) {
-                tlist[c] = list[c];
-                zt[c] = bm_test(g.keep, c) ? sv[c] : 0.0;
-              }
-            }
+          }
+        } else {
+          for (int c = tid; c < ksupp; c += nt) {
+            tlist[c] = list[c];
+            zt[c] = bm_test(g.keep, c) ? sv[c] : 0.0;
           }
         }
         __syncthreads();
@@ -223,6 +315,7 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
         for (int c = tid; c < kx; c += nt) sv[c] = zt[c];
         __syncthreads();
       }
+      GMARK(7);
       // ---- new iterate, residual, delta (solvers.py:285-290) -----------------
       for (int n = tid; n < N; n += nt) x[n] = 0.0;
       __syncthreads();
@@ -241,8 +334,41 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
       for (int c = tid; c < kx; c += nt) nf |= !isfinite(sv[c]);
       delta = sqrt(cta_sum(part, g.red));
       nf = __syncthreads_or(nf);
+      GMARK(8);
       ++iters;
       if (nf || !isfinite(delta)) { failed = true; break; }
+      if (!skipped) {
+        // mismatch mask over periods p = 2..kRing-1 against the stored states
+        int mis = 0;
+        const int hist = iters - 1 < kRing - 1 ? iters - 1 : kRing - 1;   // states stored so far
+        for (int j = tid; j < M; j += nt) {
+          const long long rb = __double_as_longlong(r[j]);
+          for (int pp = 2; pp <= hist; ++pp)
+            if (__double_as_longlong(ring[((iters - pp) % kRing) * M + j]) != rb) mis |= 1 << pp;
+        }
+        if (tid == 0) g.mis = 0;
+        __syncthreads();
+        if (mis) atomicOr(&g.mis, mis);
+        __syncthreads();
+        if (tid == 0) {
+          int per = 0;
+          for (int pp = 2; pp <= hist && !per; ++pp) {
+            if ((g.mis >> pp) & 1) continue;
+            bool same = true;
+            for (int e = 0; e < 8; ++e) same &= g.ringbm[(iters - pp) % kRing][e] == g.supp[e];
+            if (same) per = pp;
+          }
+          g.period = per;
+          for (int e = 0; e < 8; ++e) g.ringbm[iters % kRing][e] = g.supp[e];
+        }
+        for (int j = tid; j < M; j += nt) ring[(iters % kRing) * M + j] = r[j];
+        __syncthreads();
+        if (g.period) {
+          const int per = g.period;
+          iters += ((a.prm.max_iter - iters) / per) * per;
+          skipped = true;
+        }
+      }
     }
     // ---- results ----------------------------------------------------------------
     for (int n = tid; n < N; n += nt) a.x_out[pid * N + n] = failed ? 0.0 : x[n];
@@ -255,42 +381,82 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(GreedyArgs a) {
       if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - t0);
     }
     __syncthreads();
+    GMARK(10);
   }
+#ifdef HCS_PHASES
+  if (tid == 0)
+    for (int k = 0; k < 15; ++k) atomicAdd(&g_phase[k], (unsigned long long)hcs_ph[k]);
+#endif
 }
 
-size_t greedy_smem_bytes(int N, int M, int ld, bool global_ls) {
-  const int KMAX = M + 1;
-  size_t b = global_ls ? 0 : sizeof(double) * (size_t)M * ld;
-  b += sizeof(double) * (2 * kMaxN + 2 * M + 4 * (KMAX + 1));
-  b += sizeof(int) * (KMAX + 1 + 2 * kMaxN);
-  b += M + 16 + sizeof(GreedyShared);
-  (void)N;
-  return (b + 15) & ~(size_t)15;
+size_t greedy_smem_bytes(int M, int kalloc) { return greedy_layout(M, kalloc).bytes; }
+
+int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
+  int k = greedy_kalloc(algo, M, kappa);
+  while (k > 8 && greedy_layout(M, k).bytes > smem_cap) k -= 8;
+  return k;
 }
 
-cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaSuccess;
-#define HCS_LAUNCH_GREEDY(A)                                                                        \
-  e = cudaFuncSetAttribute(greedy_kernel<A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-  if (e != cudaSuccess) return e;                                                                   \
-  greedy_kernel<A><<<grid, kGreedyThreads, smem, stream>>>(args);
-  if (algo == kGomp) {
-    HCS_LAUNCH_GREEDY(kGomp)
-  } else if (algo == kBiht) {
-    HCS_LAUNCH_GREEDY(kBiht)
-  } else {
-    HCS_LAUNCH_GREEDY(kCosamp)
-  }
-#undef HCS_LAUNCH_GREEDY
+size_t greedy_ls_doubles(int M) { return (size_t)ls_doubles(M, M); }
+
+template <int ALGO, int NQ>
+static cudaError_t launch_t(const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(greedy_kernel<ALGO, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  greedy_kernel<ALGO, NQ><<<grid, kGreedyThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }
 
-int greedy_blocks_per_sm(int algo, size_t smem) {
+template <int NQ>
+static cudaError_t launch_nq(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
+  if (algo == kGomp) return launch_t<kGomp, NQ>(args, grid, smem, stream);
+  if (algo == kBiht) return launch_t<kBiht, NQ>(args, grid, smem, stream);
+  return launch_t<kCosamp, NQ>(args, grid, smem, stream);
+}
+
+cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
+  const int Mp = (args.M + 7) & ~7;
+  return Mp <= 96 ? launch_nq<3>(algo, args, grid, smem, stream) : launch_nq<8>(algo, args, grid, smem, stream);
+}
+
+template <int NQ>
+static int blocks_nq(int algo, size_t smem) {
   int nb = 0;
-  if (algo == kGomp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kGomp>, kGreedyThreads, smem);
-  else if (algo == kBiht) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kBiht>, kGreedyThreads, smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kCosamp>, kGreedyThreads, smem);
+  if (algo == kGomp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kGomp, NQ>, kGreedyThreads, smem);
+  else if (algo == kBiht) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kBiht, NQ>, kGreedyThreads, smem);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kCosamp, NQ>, kGreedyThreads, smem);
   return nb;
 }
 
+int greedy_blocks_per_sm(int algo, int M, size_t smem) {
+  // the dynamic shared-memory limit must be raised before the occupancy query
+  const int Mp = (M + 7) & ~7;
+  if (Mp <= 96) {
+    if (algo == kGomp) cudaFuncSetAttribute(greedy_kernel<kGomp, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else if (algo == kBiht) cudaFuncSetAttribute(greedy_kernel<kBiht, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else cudaFuncSetAttribute(greedy_kernel<kCosamp, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return blocks_nq<3>(algo, smem);
+  }
+  if (algo == kGomp) cudaFuncSetAttribute(greedy_kernel<kGomp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  else if (algo == kBiht) cudaFuncSetAttribute(greedy_kernel<kBiht, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  else cudaFuncSetAttribute(greedy_kernel<kCosamp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return blocks_nq<8>(algo, smem);
+}
+
 }  // namespace hcs
+
+// debug builds: per-phase cycle totals of the greedy kernel (summed over CTAs)
+extern "C" int hcs_debug_phases(unsigned long long* out16, int reset) {
+#ifdef HCS_PHASES
+  cudaMemcpyFromSymbol(out16, hcs::g_phase, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(hcs::g_phase, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return 1;
+#endif
+}

@@ -24,7 +24,7 @@ struct ConvexArgs {
 
 struct GreedyArgs {
   long long P;
-  int N, M, ld;          // ld: row stride of the LS matrix (odd, >= M + 1)
+  int N, M, kalloc;      // kalloc: LS columns the shared-memory region holds
   const double* basis;   // Psi, N x N row-major
   const double* y;
   const uint8_t* mask;
@@ -33,7 +33,7 @@ struct GreedyArgs {
   Params prm;
   unsigned long long* counter;
   int* err;
-  double* gscratch;      // non-null: LS matrices live in global memory (large M)
+  double* gscratch;      // per-CTA global LS scratch (systems beyond the shared-memory size)
 };
 
 // hcs_convex.cu
@@ -43,8 +43,10 @@ cudaError_t launch_prep_basis(const double* basis, int N, int Np, double2* fragS
                               cudaStream_t stream);
 // hcs_greedy.cu
 cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream);
-size_t greedy_smem_bytes(int N, int M, int ld, bool global_ls);
-int greedy_blocks_per_sm(int algo, size_t smem);
+size_t greedy_smem_bytes(int M, int kalloc);
+int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap);
+size_t greedy_ls_doubles(int M);
+int greedy_blocks_per_sm(int algo, int M, size_t smem);
 // hcs_batched.cu
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s,
                               int32_t* path, cudaStream_t stream);

@@ -142,3 +142,21 @@ def test_kernel_goldens(golden_dir):
         s = gk.least_squares(k[f"ls_b{i}"], k[f"ls_y{i}"])
         ref = k[f"ls_s{i}"]
         np.testing.assert_allclose(s, ref, rtol=0, atol=1e-10 * max(1.0, np.abs(ref).max()))
+
+
+def test_cosamp_cycling_tail_pixels():
+    """CoSaMP pixels that never converge enter exact 2- and 4-cycles; the GPU
+    skips whole periods (hcs_greedy.cu) and must still match the oracle's
+    2000-iteration result exactly in x, delta, iterations and flags."""
+    c = synth.generate(30, 100, 224, seed=11)
+    pick = np.array([95, 711, 757, 1068, 1297, 1984, 2086, 2149, 2213, 2543, 0, 1, 2, 3])
+    y, masks = c.y[pick], c.masks[pick]
+    cfg = SolverConfig(kappa=27, time_limit=None, max_iter=2000)
+    got = run_gpu("cosamp", y, masks, c.basis, cfg, trace=True)
+    ref = oc.solve_cube("cosamp", c.basis, y, masks, oc.OracleConfig(kappa=27, max_iter=2000), jobs=8,
+                        chunk=1, trace=True)
+    assert (ref.iterations[:10] == 2000).all() and not ref.converged[:10].any()
+    refd = dict(x=ref.x, iterations=ref.iterations, converged=ref.converged, failed_at=ref.failed_at)
+    rep = compare(refd, got, y, ref.traces, got.get("trace"), "cosamp")
+    assert not rep["bad"], rep["bad"]
+    np.testing.assert_allclose(got["final_delta"], ref.final_delta, rtol=1e-6, atol=1e-12)

@@ -65,6 +65,32 @@ __global__ void dmma16816_kernel(double* out, int iters) {
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// dependent-chain latency (one warp): cycles per DMMA / DFMA / SHFL
+__global__ void latency_kernel(long long* out, int iters, double a, double b) {
+  double c0 = threadIdx.x, c1 = 1.0;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i)
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+  long long t1 = clock64();
+  double f = c0;
+  for (int i = 0; i < iters; ++i) f = fma(f, a, b);
+  long long t2 = clock64();
+  double g = c1;
+  for (int i = 0; i < iters; ++i) g = __shfl_xor_sync(0xffffffffu, g, 1) + 1.0;
+  long long t3 = clock64();
+  double h = c0 + 1.0;
+  for (int i = 0; i < iters; ++i) h = sqrt(h) + 1.0;
+  long long t4 = clock64();
+  double q = c1 + 2.0;
+  for (int i = 0; i < iters; ++i) q = 1.0 / q + 1.5;
+  long long t5 = clock64();
+  if (threadIdx.x == 0) {
+    out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = t4 - t3; out[4] = t5 - t4;
+    out[5] = (long long)(c0 + c1 + f + g + h + q);
+  }
+}
+
 template <typename K>
 float time_kernel(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -122,6 +148,17 @@ int main() {
     printf(", \"dfma_sustained_tflops\": %.2f", flops / ms / 1e9);
   }
   CK(cudaGetLastError());
+  {
+    long long* lat;
+    CK(cudaMalloc(&lat, 8 * sizeof(long long)));
+    const int it = 4096;
+    latency_kernel<<<1, 32>>>(lat, it, 0.999, 1e-3);
+    latency_kernel<<<1, 32>>>(lat, it, 0.999, 1e-3);
+    long long h[8];
+    CK(cudaMemcpy(h, lat, sizeof(h), cudaMemcpyDeviceToHost));
+    printf(", \"lat_dmma_cyc\": %.1f, \"lat_dfma_cyc\": %.1f, \"lat_shfl_add_cyc\": %.1f, \"lat_dsqrt_add_cyc\": %.1f, \"lat_drcp_add_cyc\": %.1f",
+           (double)h[0] / it, (double)h[1] / it, (double)h[2] / it, (double)h[3] / it, (double)h[4] / it);
+  }
   printf("}\n");
   return 0;
 }

@@ -1,0 +1,64 @@
+"""Run one solver configuration on a synthetic cube slice (profiling helper).
+
+    python tools/run_case.py --cube salinas --algo cosamp --kappa 27 --pixels 8000 [--reps 3]
+"""
+
+import argparse
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2401_14762_b200 import synth  # noqa: E402
+from paper_2401_14762_b200.solvers import SolverConfig, solve_batch  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cube", default="salinas")
+    ap.add_argument("--algo", default="cosamp")
+    ap.add_argument("--kappa", type=int, default=27)
+    ap.add_argument("--lam", type=float, default=0.1)
+    ap.add_argument("--cap", type=int, default=2000)
+    ap.add_argument("--pixels", type=int, default=8000)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    n = synth.CUBES[args.cube]["n"]
+    rows = max(1, args.pixels // 100)
+    cube = synth.generate(rows, 100, n, seed=11)
+    dev = torch.device("cuda")
+    y = torch.as_tensor(cube.y, device=dev)
+    m = torch.as_tensor(cube.masks, device=dev)
+    b = torch.as_tensor(cube.basis, device=dev)
+    params = dict(kappa=args.kappa) if args.algo in ("gomp", "biht", "cosamp") else dict(lam=args.lam)
+    cfg = SolverConfig(time_limit=None, max_iter=args.cap, **params)
+    import ctypes
+    from paper_2401_14762_b200 import _native
+    lib = _native.load()
+    ph = (ctypes.c_ulonglong * 16)()
+    has_ph = hasattr(lib, "hcs_debug_phases") and lib.hcs_debug_phases(ph, 1) == 0
+    out = None
+    for _ in range(args.reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = solve_batch(args.algo, y, m, b, cfg, out=out)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        it = out.iterations.cpu().numpy()
+        print(f"{args.algo} k={args.kappa} P={cube.n_pixels}: {dt * 1e3:.2f} ms, {cube.n_pixels / dt:.0f} px/s, "
+              f"iters mean {it.mean():.2f} max {it.max()} total {it.sum()}, {dt / max(it.sum(), 1) * 1e6:.2f} us/iter")
+        if has_ph:
+            lib.hcs_debug_phases(ph, 1)
+            names = ["stop", "corr", "select", "gather", "panel", "trail", "backsub", "post", "resid", "fallback",
+                     "result"]
+            tot = sum(ph[:11])
+            print("  phases (% of CTA cycles): " + ", ".join(f"{nm} {100.0 * ph[i] / max(tot, 1):.1f}"
+                                                           for i, nm in enumerate(names)))
+
+
+if __name__ == "__main__":
+    main()
