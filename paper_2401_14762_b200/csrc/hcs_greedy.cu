@@ -31,7 +31,7 @@ __device__ unsigned long long g_phase[16];
 #endif
 
 constexpr int kGreedyThreads = 128;
-constexpr int kRing = 8;   // states kept for cycle detection (periods 2..7)
+constexpr int kRing = 32;  // state hashes kept for cycle detection (periods 2..31)
 
 struct GreedyShared {
   uint32_t supp[8], sel[8], keep[8];
@@ -39,6 +39,9 @@ struct GreedyShared {
   double Tm[128], G[64], tau[16];
   double wsc[4 * 64];
   uint32_t ringbm[kRing][8];
+  unsigned long long ringh[kRing];
+  uint32_t snapbm[8];
+  unsigned long long hpart[4];
   long long pid;
   long long start;
   int mis;
@@ -82,7 +85,7 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   L.vn2 = o; o += M + 2;
   L.zt = o; o += M + 2;
   L.keys = o; o += kMaxN;
-  L.ring = o; o += kRing * M;
+  L.ring = o; o += M;           // residual snapshot for exact cycle confirmation
   L.ints = o;
   // ints: perm (M + 2), list (256), tlist (256); then msk bytes, then GreedyShared
   size_t b = sizeof(double) * (size_t)o + sizeof(int) * (size_t)(M + 2 + 2 * kMaxN) + (size_t)M;
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
   int* tlist = list + kMaxN;    // support of the new iterate
   uint8_t* msk = reinterpret_cast<uint8_t*>(tlist + kMaxN);
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(S + L.keys);
-  double* ring = S + L.ring;    // kRing residuals (cycle detection)
+  double* snap = S + L.ring;    // residual snapshot (cycle confirmation)
   GreedyShared& g = *reinterpret_cast<GreedyShared*>(reinterpret_cast<uintptr_t>(msk + M + 15) & ~uintptr_t(15));
   const LsScratch sc{S + L.vn1, S + L.vn2, S + L.zt, perm, g.red, &g.ipiv};
   const BlockedScratch bs{yv, g.Tm, g.G, g.wsc, g.tau, S + L.zt, &g.flag};
@@ -159,12 +162,22 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
     double* B = K <= kalloc ? S : Bglob;
     const int ldb = blocked_ld(K);
     const int Kp = (K + 7) & ~7;
-    // warp w gathers rows w, w+4, ...; lanes over columns (coalesced within a Psi row)
+    // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
+    // copies rows w, w+4, ...; lanes over columns
+    const bool shared_b = K <= kalloc;
     for (int rr = warp; rr < Mp; rr += 4) {
       const double* row = a.basis + (size_t)(rr < M ? msk[rr] : 0) * N;
-      for (int c = lane; c < Kp; c += 32)
-        B[rr * ldb + c] = (rr < M && c < K) ? __ldg(row + cols[c]) : 0.0;
+      for (int c = lane; c < Kp; c += 32) {
+        double* dst = B + rr * ldb + c;
+        if (rr < M && c < K) {
+          if (shared_b) cp_async8(dst, row + cols[c]);
+          else *dst = __ldg(row + cols[c]);
+        } else {
+          *dst = 0.0;
+        }
+      }
     }
+    cp_async_wait_all();
     for (int rr = tid; rr < Mp; rr += nt) yv[rr] = rr < M ? ys[rr] : 0.0;
     __syncthreads();
     GMARK(3);
@@ -223,6 +236,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
     // are skipped, giving the same x, delta and iteration count as iterating.
     // Disabled under a wall-clock budget (timeouts depend on elapsed time).
     bool skipped = !(ALGO != kBiht && a.prm.limit_ns < 0 && a.prm.max_iter > 0);
+    int pend_p = 0, pend_t = 0;   // candidate period (hash match) awaiting exact confirmation
     for (;;) {
       // ---- stop rule before the pass (solvers.py:115-127) -------------------
       if (tid == 0) g.dec = stop_decision(delta, iters, t0, a.prm);
@@ -338,33 +352,49 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       ++iters;
       if (nf || !isfinite(delta)) { failed = true; break; }
       if (!skipped) {
-        // mismatch mask over periods p = 2..kRing-1 against the stored states
+        // 64-bit hash of the residual bits (order-aware mix, summed over rows)
+        unsigned long long h = 0ull;
         int mis = 0;
-        const int hist = iters - 1 < kRing - 1 ? iters - 1 : kRing - 1;   // states stored so far
         for (int j = tid; j < M; j += nt) {
-          const long long rb = __double_as_longlong(r[j]);
-          for (int pp = 2; pp <= hist; ++pp)
-            if (__double_as_longlong(ring[((iters - pp) % kRing) * M + j]) != rb) mis |= 1 << pp;
+          unsigned long long z = (unsigned long long)__double_as_longlong(r[j]) + 0x9E3779B97F4A7C15ull * (j + 1);
+          z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+          z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+          h += z ^ (z >> 31);
+          if (pend_p) mis |= __double_as_longlong(snap[j]) != __double_as_longlong(r[j]);
         }
-        if (tid == 0) g.mis = 0;
-        __syncthreads();
-        if (mis) atomicOr(&g.mis, mis);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+        if (lane == 0) g.hpart[warp] = h;
+        mis = __syncthreads_or(mis);
+        h = g.hpart[0] + g.hpart[1] + g.hpart[2] + g.hpart[3];
+        int per = 0;
+        if (pend_p && iters == pend_t + pend_p) {
+          // exact confirmation: the state recurred bit for bit after pend_p passes
+          bool same = !mis;
+          for (int e = 0; e < 8; ++e) same &= g.snapbm[e] == g.supp[e];
+          if (same) per = pend_p;
+          pend_p = 0;
+        }
+        if (!per && !pend_p) {
+          const int hist = iters - 1 < kRing - 1 ? iters - 1 : kRing - 1;
+          for (int pp = 2; pp <= hist && !pend_p; ++pp) {
+            const int slot = (iters - pp) % kRing;
+            if (g.ringh[slot] != h) continue;
+            bool same = true;
+            for (int e = 0; e < 8; ++e) same &= g.ringbm[slot][e] == g.supp[e];
+            if (same) { pend_p = pp; pend_t = iters; }
+          }
+          if (pend_p) {
+            for (int j = tid; j < M; j += nt) snap[j] = r[j];
+            if (tid < 8) g.snapbm[tid] = g.supp[tid];
+          }
+        }
         __syncthreads();
         if (tid == 0) {
-          int per = 0;
-          for (int pp = 2; pp <= hist && !per; ++pp) {
-            if ((g.mis >> pp) & 1) continue;
-            bool same = true;
-            for (int e = 0; e < 8; ++e) same &= g.ringbm[(iters - pp) % kRing][e] == g.supp[e];
-            if (same) per = pp;
-          }
-          g.period = per;
+          g.ringh[iters % kRing] = h;
           for (int e = 0; e < 8; ++e) g.ringbm[iters % kRing][e] = g.supp[e];
         }
-        for (int j = tid; j < M; j += nt) ring[(iters % kRing) * M + j] = r[j];
-        __syncthreads();
-        if (g.period) {
-          const int per = g.period;
+        if (per) {
           iters += ((a.prm.max_iter - iters) / per) * per;
           skipped = true;
         }

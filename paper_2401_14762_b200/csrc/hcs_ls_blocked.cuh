@@ -138,13 +138,23 @@ __device__ __forceinline__ void panel_factor(double* B, int ld, int Mp, int c0, 
   HCS_MARKP(ph, 12);
   if (!need_t) return;
   // T (dlarft 'F','C'): T[j][i] = -tau_i sum_{l=j}^{i-1} T[j][l] (V^T V)[l][i]
-  double g[2] = {0.0, 0.0};
-  for (int k0 = c0; k0 < Mp; k0 += 4) {
-    const double av = vval(B, ld, k0 + (lane & 3), c0, lane >> 2);   // A = V^T, B = V: same fragment
-    dmma8(g, av, av);
+  double g[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  {
+    int k0 = c0;
+    for (; k0 + 12 < Mp; k0 += 16) {
+      double av[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = vval(B, ld, k0 + 4 * u + (lane & 3), c0, lane >> 2);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma8(g[u], av[u], av[u]);   // A = V^T, B = V: same fragment
+    }
+    for (; k0 < Mp; k0 += 4) {
+      const double av = vval(B, ld, k0 + (lane & 3), c0, lane >> 2);
+      dmma8(g[0], av, av);
+    }
   }
-  sc.G[(lane >> 2) * 8 + 2 * (lane & 3)] = g[0];
-  sc.G[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = g[1];
+  sc.G[(lane >> 2) * 8 + 2 * (lane & 3)] = (g[0][0] + g[1][0]) + (g[2][0] + g[3][0]);
+  sc.G[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = (g[0][1] + g[1][1]) + (g[2][1] + g[3][1]);
   __syncwarp();
   if (lane < 8) {
     const int j = lane;
@@ -173,45 +183,78 @@ __device__ __forceinline__ void panel_factor(double* B, int ld, int Mp, int c0, 
 }
 
 // Apply Q_p^T (panel at c0, T slot buf) to the 8-column tile at t0 (one warp).
-__device__ __forceinline__ void tile_update(double* B, int ld, int Mp, int c0, int t0, const BlockedScratch& sc,
-                                            int buf, double* wsc) {
+// Loads are issued ahead of the DMMAs in groups of four k-steps / row blocks
+// so a single warp keeps several shared-memory loads and MMAs in flight.
+__device__ __forceinline__ void tile_update(double* __restrict__ B, int ld, int Mp, int c0, int t0,
+                                            const BlockedScratch& sc, int buf, double* __restrict__ wsc) {
   const int lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
   const double* T_b = sc.Tm + 64 * buf;
-  // W = V^T C (8 x 8, k over rows c0..Mp), two interleaved accumulator chains
-  double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+  // W = V^T C (8 x 8, k over rows c0..Mp): four accumulator chains
+  double w[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
   int k0 = c0;
-  for (; k0 + 4 < Mp; k0 += 8) {
-    const int kr0 = k0 + (lane & 3), kr1 = kr0 + 4;
-    dmma8(w0, vval(B, ld, kr0, c0, lane >> 2), B[kr0 * ld + t0 + (lane >> 2)]);
-    dmma8(w1, vval(B, ld, kr1, c0, lane >> 2), B[kr1 * ld + t0 + (lane >> 2)]);
+  for (; k0 + 12 < Mp; k0 += 16) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kr = k0 + 4 * u + lc;
+      av[u] = vval(B, ld, kr, c0, lr);
+      bv[u] = B[kr * ld + t0 + lr];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma8(w[u], av[u], bv[u]);
   }
-  if (k0 < Mp) {
-    const int kr0 = k0 + (lane & 3);
-    dmma8(w0, vval(B, ld, kr0, c0, lane >> 2), B[kr0 * ld + t0 + (lane >> 2)]);
+  for (; k0 < Mp; k0 += 4) {
+    const int kr = k0 + lc;
+    dmma8(w[0], vval(B, ld, kr, c0, lr), B[kr * ld + t0 + lr]);
   }
-  wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = w0[0] + w1[0];
-  wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = w0[1] + w1[1];
+  wsc[lr * 8 + 2 * lc] = (w[0][0] + w[1][0]) + (w[2][0] + w[3][0]);
+  wsc[lr * 8 + 2 * lc + 1] = (w[0][1] + w[1][1]) + (w[2][1] + w[3][1]);
   __syncwarp();
   // W' = T^T W
   double wp[2] = {0.0, 0.0};
 #pragma unroll
   for (int kk0 = 0; kk0 < 8; kk0 += 4) {
-    const int kk = kk0 + (lane & 3);
-    dmma8(wp, T_b[kk * 8 + (lane >> 2)], wsc[kk * 8 + (lane >> 2)]);
+    const int kk = kk0 + lc;
+    dmma8(wp, T_b[kk * 8 + lr], wsc[kk * 8 + lr]);
   }
   __syncwarp();
-  wsc[(lane >> 2) * 8 + 2 * (lane & 3)] = wp[0];
-  wsc[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = wp[1];
+  wsc[lr * 8 + 2 * lc] = wp[0];
+  wsc[lr * 8 + 2 * lc + 1] = wp[1];
   __syncwarp();
-  const double b0 = wsc[(lane & 3) * 8 + (lane >> 2)];
-  const double b1 = wsc[(4 + (lane & 3)) * 8 + (lane >> 2)];
-  // C -= V W'   (row blocks of 8 from c0)
-  for (int r0 = c0; r0 < Mp; r0 += 8) {
-    const int rr = r0 + (lane >> 2);
-    double* cp = B + rr * ld + t0 + 2 * (lane & 3);
+  const double b0 = wsc[lc * 8 + lr];
+  const double b1 = wsc[(4 + lc) * 8 + lr];
+  // C -= V W'   (row blocks of 8 from c0, four at a time)
+  int r0 = c0;
+  for (; r0 + 24 < Mp; r0 += 32) {
+    double c[4][2], v0[4], v1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = r0 + 8 * u + lr;
+      const double* cp = B + rr * ld + t0 + 2 * lc;
+      c[u][0] = cp[0];
+      c[u][1] = cp[1];
+      v0[u] = -vval(B, ld, rr, c0, lc);
+      v1[u] = -vval(B, ld, rr, c0, 4 + lc);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dmma8(c[u], v0[u], b0);
+      dmma8(c[u], v1[u], b1);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double* cp = B + (r0 + 8 * u + lr) * ld + t0 + 2 * lc;
+      cp[0] = c[u][0];
+      cp[1] = c[u][1];
+    }
+  }
+  for (; r0 < Mp; r0 += 8) {
+    const int rr = r0 + lr;
+    double* cp = B + rr * ld + t0 + 2 * lc;
     double c[2] = {cp[0], cp[1]};
-    dmma8(c, -vval(B, ld, rr, c0, lane & 3), b0);
-    dmma8(c, -vval(B, ld, rr, c0, 4 + (lane & 3)), b1);
+    dmma8(c, -vval(B, ld, rr, c0, lc), b0);
+    dmma8(c, -vval(B, ld, rr, c0, 4 + lc), b1);
     cp[0] = c[0];
     cp[1] = c[1];
   }
