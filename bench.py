@@ -200,7 +200,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2401_14762_b200 import _native
+    from paper_2401_14762_b200 import _native, parallel
     from paper_2401_14762_b200.metrics import psnr_partials
     from paper_2401_14762_b200.solvers import SolverConfig, recover_cube, solve_batch
     from paper_2401_14762_b200.transform import Dictionary
@@ -220,7 +220,7 @@ def run_ours(args):
         solvers = [s for s in solvers if label(s[0], s[1]) in keep]
     spec = synth.CUBES[cube_name]
     X = spec["x_dim"]
-    x0, x1 = rank * X // world, (rank + 1) * X // world
+    x0, x1 = parallel.row_slab(X, rank, world)
     t_gen = time.perf_counter()
     cube = synth.generate_named(cube_name, x_range=(x0, x1), workers=min(16, host_cores()))
     t_gen = time.perf_counter() - t_gen
@@ -236,10 +236,7 @@ def run_ours(args):
     stats_d = torch.zeros((nsolv, 5), dtype=torch.float64, device=dev)   # sse, conv, failed, zero, iters
     psnr_d = torch.zeros((nsolv, 2), dtype=torch.float64, device=dev)    # sse, max|ref| (this rank)
     # PSNR peak = max |reference spectra| over the whole cube: input-derived, reduced once at setup
-    peak_t = spectra_d.abs().max().reshape(1)
-    if world > 1:
-        dist.all_reduce(peak_t, op=dist.ReduceOp.MAX)
-    peak_ref = float(peak_t.item())
+    peak_ref = float(parallel.all_reduce_max(spectra_d.abs().max().reshape(1)).item())
     torch.cuda.synchronize()
 
     out = None
@@ -257,15 +254,11 @@ def run_ours(args):
                 record[i][1].record()
             out = b
             psnr_partials(spectra_d, b.x, basis_d, out=psnr_d[i])
-            ok = b.failed_at < 0
-            stats_d[i, 1] = (b.converged.bool() & ok).sum()
-            stats_d[i, 2] = (~ok).sum()
-            stats_d[i, 3] = ((b.iterations == 0) & b.converged.bool() & ok).sum()
-            stats_d[i, 4] = b.iterations[ok].sum()
+            for f, v in enumerate(parallel.local_stats(b)):
+                stats_d[i, 1 + f] = v
             launches += b.launches + 1
         stats_d[:, 0] = psnr_d[:, 0]
-        if world > 1:
-            dist.all_reduce(stats_d, op=dist.ReduceOp.SUM)   # the one data-path collective
+        parallel.all_reduce_stats(stats_d)   # the one data-path collective
         launches_per_step = launches
 
     # FP64 tensor peak of this GPU (roofline denominator)
@@ -329,14 +322,8 @@ def run_ours(args):
     total_spectra = P_total * nsolv * args.steps
     value = total_spectra / elapsed
     per_solver = {label(a, p): P_total / t for (a, p, _), t in zip(cfgs, per_cfg)}
-    quality = {}
-    for i, (a, p, _) in enumerate(cfgs):
-        sse, conv, failed, zero, iters = stats[i]
-        peak = peak_ref
-        mse = sse / (P_total * n)
-        quality[label(a, p)] = {"psnr_db": (math.inf if mse == 0 else 10 * math.log10(peak * peak / mse)),
-                                "convergence_pct": 100.0 * conv / P_total, "iterations": int(iters),
-                                "failed": int(failed)}
+    quality = {label(a, p): parallel.cube_summary(stats[i], peak_ref, P_total, n)
+               for i, (a, p, _) in enumerate(cfgs)}
 
     # ---- end to end through the public API, host (pinned) buffers ----------------
     e2e = None

@@ -1,0 +1,274 @@
+"""Reference behaviour through the public API on the GPU.
+
+Each test restates a hypercs test (`/root/reference/pkg/tests/test_solvers.py`,
+`test_kernels.py`, `test_acceptance.py`) with a real orthonormal dictionary
+(the reference's tests use complex DFT dictionaries, which the real-FP64
+device path does not take)."""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2401_14762_b200 as hcs  # noqa: E402
+from oracle import cpu_solvers as oc  # noqa: E402
+from paper_2401_14762_b200 import synth  # noqa: E402
+from paper_2401_14762_b200.transform import Dictionary  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+NO_LIMITS = dict(time_limit=None, max_iter=2000)
+
+
+def partial_dct(n, m, seed):
+    """Seeded selection of m of n orthonormal DCT-II rows (helpers.py:13-18, real basis)."""
+    mask = hcs.build_selection_mask(n, m / n, seed)
+    assert mask.m == m
+    return hcs.build_dictionary(hcs.build_dct_basis(n), mask)
+
+
+def planted(n, m, kappa, seed):
+    rng = np.random.default_rng(seed)
+    d = partial_dct(n, m, seed)
+    x0 = np.zeros(n)
+    x0[rng.choice(n, size=kappa, replace=False)] = rng.uniform(1.0, 2.0, size=kappa) * rng.choice([-1, 1], kappa)
+    return d, x0, d.matrix @ x0
+
+
+def test_identity_dictionary_closed_form():            # test_solvers.py:105-114, C4
+    d = Dictionary.from_matrix(np.eye(3))
+    y = np.array([2.0, 0.1, -3.0])
+    for solver in (hcs.fista, hcs.admm):
+        r = solver(y, d, hcs.SolverConfig(lam=0.5, epsilon=1e-10, time_limit=None, max_iter=50000))
+        assert r.converged
+        np.testing.assert_allclose(r.x, [1.5, 0.0, -2.5], atol=1e-6)
+
+
+def test_fista_and_admm_reach_the_same_objective():     # test_solvers.py:116-122, C1
+    for seed in range(5):
+        d, _, y = planted(24, 10, 4, seed)
+        for lam in (0.1, 100.0):
+            cfg = hcs.SolverConfig(lam=lam, time_limit=None, max_iter=200000)
+            h_f = hcs.lasso_objective(hcs.fista(y, d, cfg).x, y, d, lam)
+            h_a = hcs.lasso_objective(hcs.admm(y, d, cfg).x, y, d, lam)
+            assert abs(h_f - h_a) <= 1e-6 * max(1.0, abs(h_f))
+
+
+def test_admm_reports_the_primal_gap():                 # test_solvers.py:132-136
+    d, _, y = planted(16, 7, 3, 1)
+    r = hcs.admm(y, d, hcs.SolverConfig(lam=0.1, **NO_LIMITS))
+    assert r.admm_gap is not None and r.admm_gap >= 0.0
+    assert hcs.fista(y, d, hcs.SolverConfig(lam=0.1, **NO_LIMITS)).admm_gap is None
+
+
+@pytest.mark.parametrize("name", ["fista", "admm", "gomp", "biht", "cosamp"])
+def test_zero_measurements_short_circuit(name):         # test_solvers.py:138-144, 161-165
+    d = partial_dct(16, 7, 0)
+    r = hcs.SOLVERS[name](np.zeros(7), d, hcs.SolverConfig(kappa=2))
+    assert r.converged and r.iterations == 0 and r.final_delta == 0.0
+    np.testing.assert_array_equal(r.x, np.zeros(16))
+
+
+@pytest.mark.parametrize("name", ["gomp", "biht", "cosamp"])
+def test_single_atom_recovered_exactly(name):           # test_solvers.py:148-159
+    d = partial_dct(16, 7, 0)
+    x0 = np.zeros(16)
+    x0[5] = 2.5
+    r = hcs.SOLVERS[name](d.matrix @ x0, d, hcs.SolverConfig(kappa=1, atoms_per_iter=1, **NO_LIMITS))
+    assert r.converged and r.iterations <= 2
+    np.testing.assert_allclose(r.x, x0, atol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["gomp", "biht", "cosamp"])
+def test_output_never_exceeds_kappa_nonzeros(name):     # test_solvers.py:167-175, C3
+    rng = np.random.default_rng(11)
+    d = partial_dct(32, 13, 2)
+    for kappa in (1, 3, 5):
+        cfg = hcs.SolverConfig(kappa=kappa, atoms_per_iter=1, time_limit=None, max_iter=60)
+        r = hcs.SOLVERS[name](rng.standard_normal(13), d, cfg)
+        assert np.count_nonzero(r.x) <= kappa
+
+
+def test_gomp_adds_several_atoms_per_iteration():       # test_solvers.py:177-181
+    # seeds whose partial-DCT instance is exactly recoverable (the oracle recovers 0, 4, 5 of 0..5)
+    for seed in (0, 4, 5):
+        d, x0, y = planted(32, 16, 6, seed)
+        r = hcs.gomp(y, d, hcs.SolverConfig(kappa=6, atoms_per_iter=3, **NO_LIMITS))
+        assert r.converged
+        np.testing.assert_allclose(r.x, x0, atol=1e-8)
+
+
+def test_gomp_stops_when_the_support_outgrows_the_measurements():   # test_solvers.py:183-191
+    rng = np.random.default_rng(12)
+    d = partial_dct(16, 6, 3)
+    r = hcs.gomp(rng.standard_normal(6), d, hcs.SolverConfig(kappa=6, atoms_per_iter=6, time_limit=None, max_iter=500))
+    assert not r.converged and np.count_nonzero(r.x) <= 6
+
+
+def test_precondition_validation():                    # test_solvers.py:193-203
+    d = partial_dct(16, 6, 0)
+    y = np.ones(6)
+    for solver, kappa in ((hcs.gomp, 7), (hcs.biht, 7), (hcs.cosamp, 7), (hcs.cosamp, 9)):
+        with pytest.raises(ValueError):
+            solver(y, d, hcs.SolverConfig(kappa=kappa, time_limit=None))
+
+
+def test_iteration_cap_and_expired_budget():            # test_solvers.py:207-215
+    d, _, y = planted(32, 13, 4, 5)
+    r = hcs.fista(y, d, hcs.SolverConfig(lam=1e-4, time_limit=None, max_iter=1))
+    assert r.iterations == 1 and not r.converged
+    r = hcs.fista(y, d, hcs.SolverConfig(lam=0.1, time_limit=1e-12))
+    assert r.iterations == 0 and not r.converged
+    with pytest.raises(ValueError):
+        hcs.fista(np.ones(4), d, hcs.SolverConfig())
+
+
+def test_non_finite_measurements():                     # test_solvers.py:224-229 + solvers.py:227 / kernels.py:61
+    d = partial_dct(8, 3, 0)
+    y = np.array([np.nan, 1.0, 1.0])
+    with pytest.raises(hcs.NumericalFailure) as info:
+        hcs.fista(y, d, hcs.SolverConfig(lam=0.1, time_limit=None))
+    assert info.value.iteration == 1
+    for name in ("admm", "gomp", "biht", "cosamp"):     # the reference raises ValueError from scipy
+        with pytest.raises(ValueError):
+            hcs.SOLVERS[name](y, d, hcs.SolverConfig(kappa=1, time_limit=None, max_iter=10))
+
+
+def test_epsilon_above_one_converges_before_iterating():   # stop rule with delta0 = 1 (solvers.py:111)
+    d, _, y = planted(32, 13, 4, 5)
+    for name in hcs.SOLVERS:
+        r = hcs.SOLVERS[name](y, d, hcs.SolverConfig(kappa=2, epsilon=2.0, time_limit=None))
+        assert r.iterations == 0 and r.converged
+
+
+class TestRecoverCube:                                  # test_solvers.py:240-316
+    @pytest.fixture
+    def measured(self):
+        rng = np.random.default_rng(8)
+        d = partial_dct(16, 7, 1)
+        x_true = np.zeros((2, 3, 16))
+        for ix in range(2):
+            for iy in range(3):
+                x_true[ix, iy, rng.choice(16, size=2, replace=False)] = rng.uniform(1.0, 2.0, size=2)
+        return d, x_true, np.einsum("mk,xyk->xym", d.matrix, x_true)
+
+    def test_recovers_every_pixel(self, measured):
+        d, x_true, meas = measured
+        cube, st = hcs.recover_cube(meas, d, hcs.SolverConfig(kappa=2, atoms_per_iter=1, time_limit=None,
+                                                               max_iter=50), "gomp")
+        assert cube.shape == (2, 3, 16)
+        ref = oc.solve_cube("gomp", d.basis, meas.reshape(6, -1), np.tile(d.masks, (6, 1)),
+                            oc.OracleConfig(kappa=2, atoms_per_iter=1, max_iter=50))
+        np.testing.assert_allclose(cube.reshape(6, -1), ref.x, atol=1e-12)
+        # 5 of the 6 partial-DCT pixels are exactly recoverable (pixel (0, 1) is not, for the oracle too)
+        ok = np.abs(ref.x - x_true.reshape(6, -1)).max(axis=1) < 1e-8
+        assert ok.sum() == 5
+        np.testing.assert_allclose(cube.reshape(6, -1)[ok], x_true.reshape(6, -1)[ok], atol=1e-8)
+        assert (st.n_pixels, st.n_converged, st.n_failed, st.convergence_pct) == (6, 6, 0, 100.0)
+        assert st.total_iterations == sum(r.iterations for r in st.results) == ref.iterations.sum()
+
+    def test_runs_are_reproducible(self, measured):
+        d, _, meas = measured
+        cfg = hcs.SolverConfig(kappa=2, atoms_per_iter=1, time_limit=None, max_iter=50)
+        c1, _ = hcs.recover_cube(meas, d, cfg, "cosamp")
+        c2, _ = hcs.recover_cube(meas, d, cfg, "cosamp", jobs=4)
+        np.testing.assert_array_equal(c1, c2)
+
+    def test_admm_cube_uses_the_cached_factorization(self, measured):
+        d, _, meas = measured
+        cube, st = hcs.recover_cube(meas, d, hcs.SolverConfig(lam=0.05, alpha=1.8, time_limit=None,
+                                                               max_iter=5000), "admm")
+        ref = oc.solve_cube("admm", d.basis, meas.reshape(6, -1), np.tile(d.masks, (6, 1)),
+                            oc.OracleConfig(lam=0.05, alpha=1.8, max_iter=5000))
+        assert st.n_converged == int(ref.converged.sum()) == 5 and 1.8 in d._admm_factors
+        np.testing.assert_array_equal(st.iterations, ref.iterations)
+
+    def test_failed_pixels_are_flagged_not_fatal(self, measured):
+        d, _, meas = measured
+        meas = meas.copy()
+        meas[0, 1, 0] = np.nan
+        cube, st = hcs.recover_cube(meas, d, hcs.SolverConfig(lam=0.1, time_limit=None, max_iter=400), "fista")
+        assert st.n_failed == 1 and st.failed_pixels == [(0, 1, 1)]
+        assert st.results[1] is None
+        np.testing.assert_array_equal(cube[0, 1], np.zeros(16))
+        assert st.n_converged == 5
+
+    def test_zero_pixels_counted_separately(self):
+        d = partial_dct(8, 3, 0)
+        cube, st = hcs.recover_cube(np.zeros((1, 2, 3)), d, hcs.SolverConfig(kappa=1), "gomp")
+        assert st.n_zero_pixels == 2 and st.n_converged == 2 and st.total_iterations == 0
+
+    def test_input_validation(self, measured):
+        d, _, meas = measured
+        with pytest.raises(ValueError):
+            hcs.recover_cube(meas, d, hcs.SolverConfig(), "nope")
+        with pytest.raises(ValueError):
+            hcs.recover_cube(meas[:, :, :5], d, hcs.SolverConfig(), "fista")
+        with pytest.raises(ValueError):
+            hcs.recover_cube(meas[0], d, hcs.SolverConfig(), "fista")
+
+    def test_device_and_pinned_inputs(self, measured):
+        d, x_true, meas = measured
+        cfg = hcs.SolverConfig(kappa=2, atoms_per_iter=1, time_limit=None, max_iter=50)
+        ref, _ = hcs.recover_cube(meas, d, cfg, "gomp")
+        dev, _ = hcs.recover_cube(torch.as_tensor(meas, device="cuda"), d, cfg, "gomp")
+        pin, _ = hcs.recover_cube(torch.as_tensor(meas).pin_memory(), d, cfg, "gomp")
+        assert dev.is_cuda and not pin.is_cuda
+        np.testing.assert_array_equal(dev.cpu().numpy(), ref)
+        np.testing.assert_array_equal(pin.numpy(), ref)
+
+
+def test_per_pixel_dictionary_cube_matches_oracle():
+    c = synth.generate(6, 10, 154, seed=21)
+    d = Dictionary.per_pixel(c.basis, c.masks)
+    cfg = hcs.SolverConfig(kappa=22, mu=0.1, time_limit=None, max_iter=2000)
+    cube, st = hcs.recover_cube(c.y.reshape(6, 10, -1), d, cfg, "biht")
+    ref = oc.solve_cube("biht", c.basis, c.y, c.masks, oc.OracleConfig(kappa=22, mu=0.1, max_iter=2000))
+    np.testing.assert_array_equal(st.iterations, ref.iterations)
+    num = np.linalg.norm(cube.reshape(60, -1) - ref.x, axis=1)
+    assert np.all(num <= 1e-9 * np.maximum(np.linalg.norm(ref.x, axis=1), 1e-300))
+
+
+def test_unit_lipschitz_constant():                     # C5: 20 random selections, |L - 1| <= 1e-8
+    rng = np.random.default_rng(5)
+    for i, n in enumerate(rng.integers(8, 225, size=20)):
+        d = hcs.build_dictionary(hcs.build_dct_basis(int(n)), hcs.build_selection_mask(int(n), 0.4, seed=i))
+        assert abs(d.lipschitz - 1.0) <= 1e-8
+        assert abs(d.lipschitz - oc.lipschitz(d.matrix)) <= 1e-13
+
+
+class TestKernels:                                      # test_kernels.py
+    def test_soft_threshold(self):
+        np.testing.assert_allclose(hcs.soft_threshold(np.array([3.0, -1.0, 0.5, 0.0]), 1.0), [2.0, 0, 0, 0], atol=0)
+        np.testing.assert_array_equal(hcs.soft_threshold(np.array([1.0, -0.5, 0.0]), 0.0), [1.0, -0.5, 0.0])
+        with pytest.raises(ValueError):
+            hcs.soft_threshold(np.array([1.0]), -0.1)
+
+    def test_argmax_k(self):
+        np.testing.assert_array_equal(hcs.argmax_k(np.array([1.0, -5.0, 3.0]), 2), [1, 2])
+        np.testing.assert_array_equal(hcs.argmax_k(np.array([0.1, 9.0, 0.2, 8.0, 7.0]), 3), [1, 3, 4])
+        np.testing.assert_array_equal(hcs.argmax_k(np.array([2.0, -2.0, 1.0]), 1), [0])
+        np.testing.assert_array_equal(hcs.argmax_k(np.array([1.0, 3.0, 3.0, 3.0]), 2), [1, 2])
+        for k in (0, 3):
+            with pytest.raises(ValueError):
+                hcs.argmax_k(np.array([1.0, 2.0]), k)
+
+    def test_least_squares(self):
+        rng = np.random.default_rng(1)
+        b, y = rng.standard_normal((8, 3)), rng.standard_normal(8)
+        np.testing.assert_allclose(hcs.least_squares(b, y), np.linalg.solve(b.T @ b, b.T @ y), atol=1e-12)
+        b = rng.standard_normal((4, 4))
+        np.testing.assert_allclose(hcs.least_squares(b, y[:4]), np.linalg.solve(b, y[:4]), atol=1e-12)
+        col = rng.standard_normal(6)
+        s = hcs.least_squares(np.stack([col, col], axis=1), 3.0 * col)
+        np.testing.assert_allclose(s, [1.5, 1.5], atol=1e-10)
+        b = rng.standard_normal((3, 7))
+        np.testing.assert_allclose(hcs.least_squares(b, y[:3]), np.linalg.pinv(b) @ y[:3], atol=1e-10)
+        with pytest.raises(ValueError):
+            hcs.least_squares(np.ones((3, 2)), np.ones(4))
+
+    def test_residual_delta(self):
+        assert hcs.residual_delta(np.array([1.0, 1.0]), np.array([0.0, 0.0])) == pytest.approx(math.sqrt(2.0))
+        with pytest.raises(ValueError):
+            hcs.residual_delta(np.ones(2), np.ones(3))
