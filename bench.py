@@ -233,7 +233,7 @@ def run_ours(args):
     spectra_d = torch.as_tensor(cube.spectra, device=dev)
     cfgs = [(a, p, SolverConfig(time_limit=None, max_iter=cap, **p)) for a, p, cap in solvers]
     nsolv = len(cfgs)
-    stats_d = torch.zeros((nsolv, 5), dtype=torch.float64, device=dev)   # sse, conv, failed, zero, iters
+    stats_d = torch.zeros((nsolv, len(parallel.STAT_FIELDS)), dtype=torch.float64, device=dev)
     psnr_d = torch.zeros((nsolv, 2), dtype=torch.float64, device=dev)    # sse, max|ref| (this rank)
     # PSNR peak = max |reference spectra| over the whole cube: input-derived, reduced once at setup
     peak_ref = float(parallel.all_reduce_max(spectra_d.abs().max().reshape(1)).item())
@@ -306,18 +306,20 @@ def run_ours(args):
     dom = int(np.argmax(per_cfg))
     d_algo, d_params, _ = cfgs[dom]
     convex = d_algo in ("fista", "admm")
-    flops_per_iter = 4.0 * n * n if convex else 2.0 * n * n
-    iters_all = float(stats[dom, 4])
-    achieved = flops_per_iter * iters_all / per_cfg[dom] / world / 1e12
+    work_all = float(stats[dom, 5])                 # algorithmic FLOPs of that launch, all ranks
+    achieved = work_all / per_cfg[dom] / world / 1e12
     roofline = {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved, "peak": peak_tf,
                 "frac": achieved / peak_tf, "traffic": None,
                 "kernel": ("convex_kernel<%s>" if convex else "greedy_kernel<%s>") % d_algo,
                 "config": label(d_algo, d_params), "launch_ms": 1e3 * per_cfg[dom],
                 "peak_source": "FP64 DMMA m8n8k4 throughput measured on this GPU by hcs_dmma_peak_tflops "
                                "(MEASURED_PEAKS.json has no FP64 figure)",
-                "algorithmic": (f"{flops_per_iter:.0f} FLOP per pixel-iteration "
-                                f"({'4' if convex else '2'} N^2, N={n}) x {iters_all:.0f} pixel-iterations "
-                                f"(all ranks) per launch; per GPU")}
+                "algorithmic": ("4 N^2 FLOP per pixel-iteration (two N x N FP64 GEMMs)" if convex else
+                                "per pass 2NM (correlation) + LS(M,k) = 2Mk^2 - 2k^3/3 + 4Mk - k^2 per "
+                                "least-squares solve + 2Mk (residual), k from the actual supports")
+                               + f"; N={n}, M={m}; {work_all:.4g} FLOP in the launch (all ranks), per GPU",
+                "per_config_tflops": {label(a, p): float(stats[i, 5]) / per_cfg[i] / world / 1e12
+                                      for i, (a, p, _) in enumerate(cfgs)}}
 
     total_spectra = P_total * nsolv * args.steps
     value = total_spectra / elapsed

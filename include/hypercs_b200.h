@@ -82,6 +82,9 @@ typedef struct {
   double* admm_gap;      /* P: ||x - z|| (admm only; NaN for zero pixels) */
   double* lipschitz;     /* P: power-iteration constant of A_p (fista) */
   double* elapsed;       /* P: seconds the pixel spent in the solver (device clock) */
+  double* work;          /* P: algorithmic FLOPs executed for the pixel (SURVEY.md §8(d)
+                            counts: 4N^2 per convex pass; 2NM correlation + LS(M,k)
+                            + 2Mk residual per greedy pass), or NULL */
   uint64_t* trace;       /* optional selection trace (greedy): P x trace_calls x 4 words,
                             one 256-bit index bitmap per argmax_k call */
   int32_t* trace_len;    /* P: number of argmax_k calls recorded */

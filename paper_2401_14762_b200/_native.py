@@ -46,6 +46,7 @@ class HcsStats(ctypes.Structure):
         ("admm_gap", ctypes.c_void_p),
         ("lipschitz", ctypes.c_void_p),
         ("elapsed", ctypes.c_void_p),
+        ("work", ctypes.c_void_p),
         ("trace", ctypes.c_void_p),
         ("trace_len", ctypes.c_void_p),
         ("trace_calls", ctypes.c_int32),

@@ -105,7 +105,7 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   if (P == 0) return HCS_OK;
 
   hcs::Stats st{stats->iterations, stats->converged, stats->final_delta, stats->failed_at, stats->admm_gap,
-                stats->lipschitz, stats->elapsed, stats->trace, stats->trace_len,
+                stats->lipschitz, stats->elapsed, stats->work, stats->trace, stats->trace_len,
                 stats->trace ? stats->trace_calls : 0};
   // the budget in whole nanoseconds, rounded down (elapsed >= limit, solvers.py:123)
   const long long limit_ns = prm->time_limit > 0 ? (long long)(prm->time_limit * 1e9) : -1;

@@ -90,6 +90,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, doub
         a.st.failed_at[pid] = -1;
         if (a.st.admm_gap) a.st.admm_gap[pid] = __longlong_as_double(0x7ff8000000000000ll);
         if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
+        if (a.st.work) a.st.work[pid] = 0.0;
       }
       continue;
     }
@@ -106,6 +107,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, doub
         a.st.failed_at[pid] = -1;
         if (a.st.admm_gap) a.st.admm_gap[pid] = 0.0;
         if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - t0);
+        if (a.st.work) a.st.work[pid] = 0.0;
       }
       continue;
     }
@@ -157,6 +159,7 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState&
     if (admm && a.st.admm_gap)
       a.st.admm_gap[pid] = failed ? __longlong_as_double(0x7ff8000000000000ll) : sqrt(ss.gap2[s]);
     if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - ss.start[s]);
+    if (a.st.work) a.st.work[pid] = 4.0 * (double)a.N * (double)a.N * (double)it;
   }
 }
 

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
         a.st.failed_at[pid] = -1;
         if (a.st.trace_len) a.st.trace_len[pid] = 0;
         if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
+        if (a.st.work) a.st.work[pid] = 0.0;
       }
       __syncthreads();
       continue;
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
     // Disabled under a wall-clock budget (timeouts depend on elapsed time).
     bool skipped = !(ALGO != kBiht && a.prm.limit_ns < 0 && a.prm.max_iter > 0);
     int pend_p = 0, pend_t = 0;   // candidate period (hash match) awaiting exact confirmation
+    double work = 0.0;            // algorithmic FLOPs executed (thread 0's tally)
     for (;;) {
       // ---- stop rule before the pass (solvers.py:115-127) -------------------
       if (tid == 0) g.dec = stop_decision(delta, iters, t0, a.prm);
@@ -284,9 +286,11 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       }
       __syncthreads();
       GMARK(2);
+      work += 2.0 * N * M;                       // correlation
       if (g.brk) break;                          // keep the last iterate, no count
       ksupp = g.count;
       solve(list, ksupp);
+      work += ls_flops(M, ksupp);
       int kx;          // support size of the new iterate, indices in tlist, values in sv
       if (ALGO == kGomp) {
         // x = scatter(s); top = argmax_k(x, kappa) over all N; refit on top
@@ -300,6 +304,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
         __syncthreads();
         kx = a.prm.kappa;
         solve(tlist, kx);
+        work += ls_flops(M, kx);
       } else {
         // keep = argmax_k(s, min(kappa, k)); zero (biht) or drop (cosamp) the rest
         const int kk = a.prm.kappa < ksupp ? a.prm.kappa : ksupp;
@@ -347,6 +352,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       }
       for (int c = tid; c < kx; c += nt) nf |= !isfinite(sv[c]);
       delta = sqrt(cta_sum(part, g.red));
+      work += 2.0 * M * kx;                      // residual
       nf = __syncthreads_or(nf);
       GMARK(8);
       ++iters;
@@ -409,6 +415,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       a.st.failed_at[pid] = failed ? iters : -1;
       if (a.st.trace_len) a.st.trace_len[pid] = ncall;
       if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - t0);
+      if (a.st.work) a.st.work[pid] = work;
     }
     __syncthreads();
     GMARK(10);

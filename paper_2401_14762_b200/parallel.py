@@ -15,7 +15,7 @@ gloo on CPU for the tests.
 
 import math
 
-STAT_FIELDS = ("sse", "n_converged", "n_failed", "n_zero_pixels", "total_iterations")
+STAT_FIELDS = ("sse", "n_converged", "n_failed", "n_zero_pixels", "total_iterations", "work_flops")
 
 
 def row_slab(x_dim, rank, world):
@@ -26,21 +26,23 @@ def row_slab(x_dim, rank, world):
 
 
 def local_stats(batch, ok_mask=None):
-    """[n_converged, n_failed, n_zero_pixels, total_iterations] of one
-    DeviceBatch (or any object with iterations/converged/failed_at tensors),
-    as in RecoveryStats (solvers.py:503-513)."""
+    """[n_converged, n_failed, n_zero_pixels, total_iterations, work] of one
+    DeviceBatch (or any object with iterations/converged/failed_at tensors and
+    optionally work), as in RecoveryStats (solvers.py:503-513)."""
     ok = batch.failed_at < 0
     conv = batch.converged.bool()
+    work = getattr(batch, "work", None)
     return [
         (conv & ok).sum(),
         (~ok).sum(),
         ((batch.iterations == 0) & conv & ok).sum(),
         batch.iterations[ok].sum(),
+        work.sum() if work is not None else 0.0,
     ]
 
 
 def all_reduce_stats(stats, group=None):
-    """Sum a (configs, 5) float64 tensor of STAT_FIELDS over all ranks in place."""
+    """Sum a (configs, len(STAT_FIELDS)) float64 tensor over all ranks in place."""
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
@@ -56,7 +58,7 @@ def all_reduce_max(t, group=None):
 
 def cube_summary(row, peak, n_pixels, n_bands):
     """Cube-level numbers from one reduced STAT_FIELDS row (metrics.py:30-64)."""
-    sse, conv, failed, zero, iters = (float(v) for v in row)
+    sse, conv, failed, zero, iters = (float(v) for v in row[:5])
     mse = sse / (n_pixels * n_bands)
     return {
         "psnr_db": math.inf if mse == 0 else 10.0 * math.log10(peak * peak / mse),

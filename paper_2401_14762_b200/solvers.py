@@ -152,6 +152,7 @@ class DeviceBatch:
     admm_gap: object     # (P,) float64
     lipschitz: object    # (P,) float64
     elapsed: object      # (P,) float64
+    work: object = None  # (P,) float64 algorithmic FLOPs executed
     trace: object = None
     trace_len: object = None
     workspace: object = None
@@ -192,11 +193,13 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
         admm_gap=torch.full((P,), math.nan, **f64),
         lipschitz=torch.full((P,), math.nan, **f64),
         elapsed=torch.empty((P,), **f64),
+        work=torch.empty((P,), **f64),
     )
     st = nat.HcsStats(iterations=out.iterations.data_ptr(), converged=out.converged.data_ptr(),
                       final_delta=out.final_delta.data_ptr(), failed_at=out.failed_at.data_ptr(),
                       admm_gap=out.admm_gap.data_ptr(), lipschitz=out.lipschitz.data_ptr(),
-                      elapsed=out.elapsed.data_ptr(), trace=None, trace_len=None, trace_calls=0)
+                      elapsed=out.elapsed.data_ptr(), work=out.work.data_ptr(), trace=None, trace_len=None,
+                      trace_calls=0)
     if trace_calls > 0:
         out.trace = torch.zeros((P, trace_calls, 4), dtype=torch.int64, device=dev)
         out.trace_len = torch.zeros((P,), dtype=torch.int32, device=dev)

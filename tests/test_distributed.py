@@ -45,7 +45,7 @@ def _worker(rank, world, port, X, Y, out):
     x0, x1 = parallel.row_slab(X, rank, world)
     sl = slice(x0 * Y, x1 * Y)
     b = _Batch(it[sl], conv[sl], failed[sl])
-    stats = torch.zeros((1, 5), dtype=torch.float64)
+    stats = torch.zeros((1, len(parallel.STAT_FIELDS)), dtype=torch.float64)
     stats[0, 0] = float(sq[sl].sum())
     for f, v in enumerate(parallel.local_stats(b)):
         stats[0, 1 + f] = v
@@ -77,14 +77,14 @@ def test_gloo_world2_reduction_matches_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, X, Y, q)) for r in range(2)]
     for p in procs:
         p.start()
-    stats, peak, _ = q.get(timeout=120)
+    stats, peak, _ = q.get(timeout=90)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     it, conv, failed, sq = _fake_results(X * Y)
     ok = failed < 0
     expect = [sq.sum(), (conv.astype(bool) & ok).sum(), (~ok).sum(),
-              ((it == 0) & conv.astype(bool) & ok).sum(), it[ok].sum()]
+              ((it == 0) & conv.astype(bool) & ok).sum(), it[ok].sum(), 0.0]
     np.testing.assert_allclose(stats[0], expect, rtol=1e-12)
     assert peak == pytest.approx(sq.max())
     summ = parallel.cube_summary(stats[0], 1.0, X * Y, 4)
