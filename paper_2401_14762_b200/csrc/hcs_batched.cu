@@ -6,7 +6,7 @@
 #include "hcs_gemm.cuh"
 #include "hcs_internal.cuh"
 #include "hcs_ls.cuh"
-#include "hcs_ls_blocked.cuh"
+#include "hcs_ls_csne.cuh"
 
 namespace hcs {
 
@@ -58,37 +58,35 @@ cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t*
   return cudaGetLastError();
 }
 
-// one CTA per system; b_p row-major M x K, y_p length M.  Blocked DMMA
-// Householder first (path 0), the exact pivoted restatement when its rank
-// guard trips (path 0 if that is full rank, 1 for the minimum-norm fallback).
+// one CTA per system; b_p row-major M x K, y_p length M.  CSNE first (path 0),
+// the exact pivoted restatement when a guard trips (path 0 if that is full
+// rank, 1 for the minimum-norm fallback).
 struct LsShared {
-  double red[16], Tm[64], G[64], tau[8], wsc[4 * 64];
+  double red[16];
   int ipiv, flag;
 };
 
 __host__ __device__ inline size_t ls_batched_doubles(int M, int K) {
-  const int Mp = (M + 7) & ~7;
-  const size_t blk = (size_t)Mp * blocked_ld(K), piv = (size_t)M * ((K + 1) | 1);
+  const size_t blk = (size_t)csne_ld(M) * csne_cols(K), piv = (size_t)M * ((K + 1) | 1);
   return blk > piv ? blk : piv;
 }
 
-template <int NQ>
 __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, const double* __restrict__ b,
                                                  const double* __restrict__ y, double* __restrict__ s,
                                                  int32_t* __restrict__ path) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int Mp = (M + 7) & ~7;
   double* B = reinterpret_cast<double*>(smraw);
-  double* yv = B + ls_batched_doubles(M, K);
-  double* sv = yv + Mp;
-  double* vn1 = sv + K + 1;
-  double* vn2 = vn1 + K + 1;
-  double* zt = vn2 + K + 1;
-  LsShared* sh = reinterpret_cast<LsShared*>(zt + K + 1);
+  double* G = B + ls_batched_doubles(M, K);
+  double* rv = G + csne_gram_doubles(K);
+  double* sv = rv + M + 1;
+  double* vn1 = sv + K + 9;
+  double* vn2 = vn1 + K + 9;
+  double* zt = vn2 + K + 9;
+  LsShared* sh = reinterpret_cast<LsShared*>(zt + K + 9);
   int* perm = reinterpret_cast<int*>(sh + 1);
   const LsScratch sc{vn1, vn2, zt, perm, sh->red, &sh->ipiv};
-  const BlockedScratch bs{yv, sh->Tm, sh->G, sh->wsc, sh->tau, zt, &sh->flag};
-  const int ldb = blocked_ld(K), Kp = (K + 7) & ~7, ldp = (K + 1) | 1;
+  const CsneScratch cs{G, vn1, vn2, rv, sh->red, &sh->flag};
+  const int ldb = csne_ld(M), nc = csne_cols(K), ldp = (K + 1) | 1;
 #ifdef HCS_PHASES
   long long hcs_ph[16] = {0};
   hcs_ph[15] = clock64();
@@ -100,14 +98,15 @@ __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, cons
     int pth = 0;
     bool done = false;
     if (M >= K) {
-      for (int idx = threadIdx.x; idx < Mp * Kp; idx += blockDim.x) {
-        const int rr = idx / Kp, c = idx - rr * Kp;
-        B[rr * ldb + c] = (rr < M && c < K) ? b[(p * M + rr) * K + c] : 0.0;
+      for (int idx = threadIdx.x; idx < ldb * nc; idx += blockDim.x) {
+        const int c = idx / ldb, rr = idx - c * ldb;
+        double v = 0.0;
+        if (rr < M) v = c < K ? b[(p * M + rr) * K + c] : (c == K ? y[p * M + rr] : 0.0);
+        B[idx] = v;
       }
-      for (int rr = threadIdx.x; rr < Mp; rr += blockDim.x) yv[rr] = rr < M ? y[p * M + rr] : 0.0;
       __syncthreads();
       HCS_MARKP(php, 3);
-      done = ls_blocked<NQ>(B, ldb, M, K, sv, bs, php);
+      done = ls_csne(B, ldb, M, K, sv, cs, php);
     }
     if (!done) {
       for (int idx = threadIdx.x; idx < M * (K + 1); idx += blockDim.x) {
@@ -130,21 +129,13 @@ __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, cons
 
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s, int32_t* path,
                               cudaStream_t stream) {
-  const int Mp = (M + 7) & ~7;
-  const size_t smem = sizeof(double) * (ls_batched_doubles(M, K) + Mp + 4 * (K + 1)) + sizeof(LsShared) +
-                      sizeof(int) * (K + 2);
+  const size_t smem = sizeof(double) * (ls_batched_doubles(M, K) + csne_gram_doubles(K) + M + 1 + 4 * (K + 9)) +
+                      sizeof(LsShared) + sizeof(int) * (K + 2);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   long long blocks = P < 148 * 4 ? P : 148 * 4;
-  cudaError_t e;
-  if (Mp <= 96) {
-    e = cudaFuncSetAttribute(ls_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    ls_kernel<3><<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
-  } else {
-    e = cudaFuncSetAttribute(ls_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    ls_kernel<8><<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
-  }
+  cudaError_t e = cudaFuncSetAttribute(ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  ls_kernel<<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
   return cudaGetLastError();
 }
 

@@ -13,16 +13,16 @@
 //   * support sets as 256-bit bitmaps; union = OR, sorted list = ballot/popc;
 //   * the support-outgrew-m break happens before the solve and without
 //     counting the iteration (solvers.py:274-276, 320-321, 372-373);
-//   * least squares on the gathered M x k dictionary columns: blocked
-//     Householder on DMMA tensor cores (hcs_ls_blocked.cuh), falling back to
-//     the exact column-pivoted restatement (hcs_ls.cuh) when the rank guard
-//     trips;
+//   * least squares on the gathered M x k dictionary columns: corrected
+//     semi-normal equations with a DMMA Gram and blocked Cholesky
+//     (hcs_ls_csne.cuh), falling back to the exact column-pivoted restatement
+//     (hcs_ls.cuh) when a guard trips;
 //   * residual y - A x recomputed from Psi rows, delta and the stop rule.
 // Optional trace: the 256-bit bitmap of every argmax_k call, for the parity
 // harness's tie classification.
 #include "hcs_internal.cuh"
 #include "hcs_ls.cuh"
-#include "hcs_ls_blocked.cuh"
+#include "hcs_ls_csne.cuh"
 
 namespace hcs {
 
@@ -36,8 +36,6 @@ constexpr int kRing = 32;  // state hashes kept for cycle detection (periods 2..
 struct GreedyShared {
   uint32_t supp[8], sel[8], keep[8];
   double red[16];
-  double Tm[128], G[64], tau[16];
-  double wsc[4 * 64];
   uint32_t ringbm[kRing][8];
   unsigned long long ringh[kRing];
   uint32_t snapbm[8];
@@ -54,19 +52,21 @@ struct GreedyShared {
 };
 
 // Shared-memory layout (doubles unless noted), identical on host and device.
-// The LS matrix region holds systems of up to `kalloc` columns; larger
-// systems (rare: gOMP supports beyond kalloc) use the CTA's global scratch.
+// The LS region holds systems of up to `kalloc` columns (B and its Gram);
+// larger systems (rare: gOMP supports beyond kalloc) use the CTA's global
+// scratch.
 struct GreedyLayout {
-  int Mp, bmax;              // padded rows; doubles reserved for the LS matrix
-  int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring;   // double offsets
+  int Mp, bmax, gmax;        // padded rows; doubles for B and for the Gram tiles
+  int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring, dinv, cv;   // double offsets
   int ints;                  // int region offset (in doubles)
   size_t bytes;
 };
 
+// doubles for B: the CSNE layout (column-major, y appended) or the pivoted
+// fallback's row-major M x (K+1)|1, whichever is larger
 __host__ __device__ inline int ls_doubles(int M, int K) {
-  const int Mp = (M + 7) & ~7;
   const int piv = M * ((K + 1) | 1);
-  const int blk = Mp * blocked_ld(K);
+  const int blk = csne_ld(M) * csne_cols(K);
   return piv > blk ? piv : blk;
 }
 
@@ -74,7 +74,9 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   GreedyLayout L;
   L.Mp = (M + 7) & ~7;
   L.bmax = ls_doubles(M, kalloc);
-  int o = L.bmax;
+  if (L.bmax < 4 * kMaxN) L.bmax = 4 * kMaxN;     // also the correlation / residual scratch
+  L.gmax = csne_gram_doubles(kalloc);
+  int o = L.bmax + L.gmax;
   L.vec = o; o += kMaxN;
   L.x = o; o += kMaxN;
   L.ys = o; o += M;
@@ -84,6 +86,9 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   L.vn1 = o; o += M + 2;
   L.vn2 = o; o += M + 2;
   L.zt = o; o += M + 2;
+  L.dinv = o; o += M + 9;
+  L.cv = o; o += M + 9;
+  o = (o + 1) & ~1;             // 16-byte alignment for the paired key loads
   L.keys = o; o += kMaxN;
   L.ring = o; o += M;           // residual snapshot for exact cycle confirmation
   L.ints = o;
@@ -120,7 +125,7 @@ __device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, int* list) {
   return base;
 }
 
-template <int ALGO, int NQ>
+template <int ALGO>
 __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int N = a.N, M = a.M;
@@ -128,7 +133,8 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
   const int kalloc = a.kalloc;
   const GreedyLayout L = greedy_layout(M, kalloc);
   double* S = reinterpret_cast<double*>(smraw);
-  double* Bglob = a.gscratch + (size_t)blockIdx.x * ls_doubles(M, M);
+  double* Bglob = a.gscratch + (size_t)blockIdx.x * (ls_doubles(M, M) + csne_gram_doubles(M));
+  double* Gglob = Bglob + ls_doubles(M, M);
   double* vec = S + L.vec;      // N: p / u / x_full
   double* x = S + L.x;          // N: current iterate
   double* ys = S + L.ys;        // M
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
   double* snap = S + L.ring;    // residual snapshot (cycle confirmation)
   GreedyShared& g = *reinterpret_cast<GreedyShared*>(reinterpret_cast<uintptr_t>(msk + M + 15) & ~uintptr_t(15));
   const LsScratch sc{S + L.vn1, S + L.vn2, S + L.zt, perm, g.red, &g.ipiv};
-  const BlockedScratch bs{yv, g.Tm, g.G, g.wsc, g.tau, S + L.zt, &g.flag};
+  int* lsflag = &g.flag;
   const double NaN = __longlong_as_double(0x7ff8000000000000ll);
   const int Mp = L.Mp;
 #ifdef HCS_PHASES
@@ -159,29 +165,30 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
   // least squares on the dictionary columns `cols[0..K)` (+ y): blocked DMMA
   // Householder, exact pivoted restatement when the rank guard trips
   auto solve = [&](const int* cols, int K) {
-    double* B = K <= kalloc ? S : Bglob;
-    const int ldb = blocked_ld(K);
-    const int Kp = (K + 7) & ~7;
-    // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
-    // copies rows w, w+4, ...; lanes over columns
     const bool shared_b = K <= kalloc;
-    for (int rr = warp; rr < Mp; rr += 4) {
-      const double* row = a.basis + (size_t)(rr < M ? msk[rr] : 0) * N;
-      for (int c = lane; c < Kp; c += 32) {
-        double* dst = B + rr * ldb + c;
+    double* B = shared_b ? S : Bglob;
+    const int ldb = csne_ld(M);                  // column-major; y is column K
+    const int nc = csne_cols(K);
+    // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
+    // copies columns w, w+4, ...; lanes over rows (consecutive shared words)
+    for (int c = warp; c < nc; c += 4) {
+      const int col = c < K ? cols[c] : 0;
+      for (int rr = lane; rr < ldb; rr += 32) {
+        double* dst = B + c * ldb + rr;
         if (rr < M && c < K) {
-          if (shared_b) cp_async8(dst, row + cols[c]);
-          else *dst = __ldg(row + cols[c]);
+          const double* src = a.basis + (size_t)msk[rr] * N + col;
+          if (shared_b) cp_async8(dst, src);
+          else *dst = __ldg(src);
         } else {
-          *dst = 0.0;
+          *dst = (rr < M && c == K) ? ys[rr] : 0.0;
         }
       }
     }
     cp_async_wait_all();
-    for (int rr = tid; rr < Mp; rr += nt) yv[rr] = rr < M ? ys[rr] : 0.0;
     __syncthreads();
     GMARK(3);
-    if (ls_blocked<NQ>(B, ldb, M, K, sv, bs, php)) return;
+    const CsneScratch cs{shared_b ? S + L.bmax : Gglob, S + L.dinv, S + L.cv, yv, g.red, lsflag};
+    if (ls_csne(B, ldb, M, K, sv, cs, php)) return;
     const int ldp = (K + 1) | 1;
     for (int idx = tid; idx < M * (K + 1); idx += nt) {
       const int rr = idx / (K + 1), c = idx - rr * (K + 1);
@@ -247,18 +254,31 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       GMARK(0);
       if (dec != kContinue) { converged = dec == kConverged; break; }
       // ---- correlation / gradient proxy over all bands ----------------------
-      for (int n = tid; n < N; n += nt) {
-        double p0 = 0.0, p1 = 0.0;
-        int j = 0;
-#pragma unroll 4
-        for (; j + 1 < M; j += 2) {
-          p0 += r[j] * __ldg(a.basis + (size_t)msk[j] * N + n);
-          p1 += r[j + 1] * __ldg(a.basis + (size_t)msk[j + 1] * N + n);
+      // p = A^T r = sum_j r_j Psi[mask_j, :]: warp w takes rows j = w, w+4, ...,
+      // lanes take bands (coalesced Psi row segments, 7 independent loads per
+      // row in flight); the four warp partials are summed through shared memory
+      {
+        double* part = S;          // the LS region is free outside solve()
+        double acc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+#pragma unroll 2
+        for (int j = warp; j < M; j += 4) {
+          const double rj = r[j];
+          const double* row = a.basis + (size_t)msk[j] * N + lane;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (lane + 32 * c < N) acc[c] += rj * __ldg(row + 32 * c);
         }
-        if (j < M) p0 += r[j] * __ldg(a.basis + (size_t)msk[j] * N + n);
-        double p = p0 + p1;
-        if (ALGO == kBiht) p = __dadd_rn(x[n], __dmul_rn(a.prm.mu, p));   // solvers.py:318
-        vec[n] = p;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (lane + 32 * c < N) part[warp * kMaxN + lane + 32 * c] = acc[c];
+        __syncthreads();
+        for (int n = tid; n < N; n += nt) {
+          double p = (part[n] + part[kMaxN + n]) + (part[2 * kMaxN + n] + part[3 * kMaxN + n]);
+          if (ALGO == kBiht) p = __dadd_rn(x[n], __dmul_rn(a.prm.mu, p));   // solvers.py:318
+          vec[n] = p;
+        }
       }
       __syncthreads();
       GMARK(1);
@@ -339,13 +359,32 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
       for (int n = tid; n < N; n += nt) x[n] = 0.0;
       __syncthreads();
       for (int c = tid; c < kx; c += nt) x[tlist[c]] = sv[c];
+      // A x over the kx support columns: lanes own rows, warps split the columns
+      {
+        double* part = S;          // free again after solve()
+        double ax[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ax[q] = 0.0;
+        for (int c = warp; c < kx; c += 4) {
+          const int col = tlist[c];
+          const double sc_ = sv[c];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int j = lane + 32 * q;
+            if (j < M) ax[q] += __ldg(a.basis + (size_t)msk[j] * N + col) * sc_;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (lane + 32 * q < M) part[warp * kMaxN + lane + 32 * q] = ax[q];
+      }
+      __syncthreads();
       double part = 0.0;
       int nf = 0;
       for (int j = tid; j < M; j += nt) {
-        const double* row = a.basis + (size_t)msk[j] * N;
-        double ax = 0.0;
-        for (int c = 0; c < kx; ++c) ax += __ldg(row + tlist[c]) * sv[c];
-        const double rn = ys[j] - ax;
+        const double* pp = S + j;
+        const double axj = (pp[0] + pp[kMaxN]) + (pp[2 * kMaxN] + pp[3 * kMaxN]);
+        const double rn = ys[j] - axj;
         const double d = rn - r[j];
         part += d * d;
         r[j] = rn;
@@ -434,50 +473,36 @@ int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
   return k;
 }
 
-size_t greedy_ls_doubles(int M) { return (size_t)ls_doubles(M, M); }
+size_t greedy_ls_doubles(int M) { return (size_t)ls_doubles(M, M) + (size_t)csne_gram_doubles(M); }
 
-template <int ALGO, int NQ>
+template <int ALGO>
 static cudaError_t launch_t(const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(greedy_kernel<ALGO, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  greedy_kernel<ALGO, NQ><<<grid, kGreedyThreads, smem, stream>>>(args);
+  greedy_kernel<ALGO><<<grid, kGreedyThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }
 
-template <int NQ>
-static cudaError_t launch_nq(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  if (algo == kGomp) return launch_t<kGomp, NQ>(args, grid, smem, stream);
-  if (algo == kBiht) return launch_t<kBiht, NQ>(args, grid, smem, stream);
-  return launch_t<kCosamp, NQ>(args, grid, smem, stream);
-}
-
 cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  const int Mp = (args.M + 7) & ~7;
-  return Mp <= 96 ? launch_nq<3>(algo, args, grid, smem, stream) : launch_nq<8>(algo, args, grid, smem, stream);
+  if (algo == kGomp) return launch_t<kGomp>(args, grid, smem, stream);
+  if (algo == kBiht) return launch_t<kBiht>(args, grid, smem, stream);
+  return launch_t<kCosamp>(args, grid, smem, stream);
 }
 
-template <int NQ>
-static int blocks_nq(int algo, size_t smem) {
+template <int ALGO>
+static int blocks_t(size_t smem) {
+  // the dynamic shared-memory limit must be raised before the occupancy query
+  cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int nb = 0;
-  if (algo == kGomp) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kGomp, NQ>, kGreedyThreads, smem);
-  else if (algo == kBiht) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kBiht, NQ>, kGreedyThreads, smem);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<kCosamp, NQ>, kGreedyThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<ALGO>, kGreedyThreads, smem);
   return nb;
 }
 
 int greedy_blocks_per_sm(int algo, int M, size_t smem) {
-  // the dynamic shared-memory limit must be raised before the occupancy query
-  const int Mp = (M + 7) & ~7;
-  if (Mp <= 96) {
-    if (algo == kGomp) cudaFuncSetAttribute(greedy_kernel<kGomp, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else if (algo == kBiht) cudaFuncSetAttribute(greedy_kernel<kBiht, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else cudaFuncSetAttribute(greedy_kernel<kCosamp, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return blocks_nq<3>(algo, smem);
-  }
-  if (algo == kGomp) cudaFuncSetAttribute(greedy_kernel<kGomp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  else if (algo == kBiht) cudaFuncSetAttribute(greedy_kernel<kBiht, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  else cudaFuncSetAttribute(greedy_kernel<kCosamp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return blocks_nq<8>(algo, smem);
+  (void)M;
+  if (algo == kGomp) return blocks_t<kGomp>(smem);
+  if (algo == kBiht) return blocks_t<kBiht>(smem);
+  return blocks_t<kCosamp>(smem);
 }
 
 }  // namespace hcs

@@ -46,7 +46,7 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
 
 // Solve; s[0..K) receives the solution (shared memory).  Returns 0 for the
 // QR path, 1 for the minimum-norm fallback.  Ends with __syncthreads().
-__device__ inline int ls_solve(double* B, int ld, int M, int K, double* s, const LsScratch& sc) {
+static __device__ __noinline__ int ls_solve(double* B, int ld, int M, int K, double* s, const LsScratch& sc) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int kk = M < K ? M : K;
   const double tol3z = 1.0536712127723509e-08;  // dlaqp2 TOL3Z = sqrt(dlamch('Epsilon')) = sqrt(2^-53)

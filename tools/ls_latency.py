@@ -11,8 +11,8 @@ from paper_2401_14762_b200 import _native
 LIB = _native.load()
 PH = (ctypes.c_ulonglong * 16)()
 HAS_PH = LIB.hcs_debug_phases_ls(PH, 1) == 0
-NAMES = {3: "gather", 4: "panel0", 11: "w0-tile", 12: "panel", 13: "T", 14: "sync-wait", 5: "loop-end",
-         6: "backsub", 10: "out"}
+NAMES = {3: "gather", 4: "gram", 11: "diag0", 12: "panels", 13: "trail+diag", 5: "chol-end", 6: "solve+refine",
+         10: "out"}
 
 
 def run(M, K, P, reps=5):
