@@ -81,6 +81,23 @@ def soft_threshold(v, t):
     return v * scale
 
 
+TIE_REL = 1e-12   # roundoff-degenerate selection: max|v| or k-th gap <= TIE_REL * ||y||
+
+
+class Recorder(list):
+    """Selection trace; with ``force`` it also implements the forced-selection
+    replay of SURVEY.md §8(c): at a call whose own selection is
+    roundoff-degenerate (max|v| or the k-th gap <= TIE_REL * ||y||) the
+    selection recorded by the candidate implementation (force[call index]) is
+    used instead of the oracle's own."""
+
+    def __init__(self, force=None, ynorm=0.0):
+        super().__init__()
+        self.force = force or {}
+        self.ynorm = ynorm
+        self.forced = 0
+
+
 def argmax_k(v, k, trace=None):
     """kernels.py:31-41: k largest |v|, ties to the lowest index, ascending."""
     v = np.asarray(v)
@@ -92,7 +109,14 @@ def argmax_k(v, k, trace=None):
     if trace is not None:
         srt = mag[order]
         gap = float(srt[k - 1] - srt[k]) if k < v.size else math.inf
-        trace.append((k, tuple(int(i) for i in picked), float(srt[0]), gap))
+        vmax = float(srt[0])
+        if isinstance(trace, Recorder) and len(trace) in trace.force:
+            lim = TIE_REL * trace.ynorm
+            forced = tuple(int(i) for i in trace.force[len(trace)])
+            if (vmax <= lim or gap <= lim) and len(forced) == k:
+                picked = np.array(forced, dtype=np.intp)
+                trace.forced += 1
+        trace.append((k, tuple(int(i) for i in picked), vmax, gap))
     return picked
 
 

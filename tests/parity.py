@@ -51,9 +51,19 @@ def degenerate(entry, ynorm):
     return vmax <= TIE * ynorm or gap <= TIE * ynorm
 
 
-def compare(ref, cand, y, ref_traces=None, cand_traces=None, algo=""):
+def replay_matches(res, cand, p):
+    """Forced-selection replay result vs the candidate pixel p."""
+    return (int(res.iterations) == int(cand["iterations"][p]) and bool(res.converged) == bool(cand["converged"][p])
+            and int(res.failed_at) == int(cand["failed_at"][p]) and coef_ok(cand["x"][p], res.x)
+            and np.array_equal(significant(cand["x"][p]), significant(res.x)))
+
+
+def compare(ref, cand, y, ref_traces=None, cand_traces=None, algo="", replay=None):
     """ref/cand: dicts with x, iterations, converged, failed_at arrays.
 
+    ``replay(p, force)`` (optional) re-runs the oracle on pixel p with the
+    candidate's selections forced at roundoff-degenerate calls; a tie
+    exception is only accepted if that replay reproduces the candidate.
     Returns a report dict; ``report["bad"]`` lists real mismatches."""
     P = len(ref["iterations"])
     bad, ties, worst = [], [], 0.0
@@ -76,7 +86,14 @@ def compare(ref, cand, y, ref_traces=None, cand_traces=None, algo=""):
             if cand_traces is not None:
                 i = first_divergence(tr, cand_traces[p])
                 if i is not None and i < len(tr) and degenerate(tr[i], ynorm):
-                    ties.append(dict(why, call=i, vmax=tr[i][2] / ynorm, gap=tr[i][3] / ynorm))
+                    entry = dict(why, call=i, vmax=tr[i][2] / ynorm, gap=tr[i][3] / ynorm)
+                    if replay is not None:
+                        force = {c: tuple(e[1]) for c, e in enumerate(cand_traces[p])}
+                        entry["replay_ok"] = replay_matches(replay(p, force), cand, p)
+                        if not entry["replay_ok"]:
+                            bad.append(dict(entry, reason="forced-selection replay does not reproduce"))
+                            continue
+                    ties.append(entry)
                     continue
             elif any(degenerate(e, ynorm) for e in tr):
                 ties.append(dict(why, call=-1))

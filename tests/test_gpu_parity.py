@@ -59,6 +59,14 @@ def run_gpu(algo, y, masks, basis, cfg, trace=False):
     return res
 
 
+def make_replay(algo, basis, y, masks, ocfg):
+    """Forced-selection replay of SURVEY.md §8(c) through the oracle."""
+    def replay(p, force):
+        rec = oc.Recorder(force=force, ynorm=float(np.linalg.norm(np.nan_to_num(y[p]))))
+        return oc.solve_pixel(algo, y[p], basis[np.asarray(masks[p]).astype(np.intp), :], ocfg, trace=rec)
+    return replay
+
+
 def load_case(golden_dir, name):
     z = np.load(golden_dir / f"{name}.npz", allow_pickle=False)
     return z, json.loads(str(z["meta"]))
@@ -73,8 +81,9 @@ def test_gpu_matches_reference_golden(golden_dir, name):
     greedy = algo in ("gomp", "biht", "cosamp")
     got = run_gpu(algo, z["y"], z["masks"], basis, cfg, trace=greedy)
     ref = dict(x=z["x"], iterations=z["iterations"], converged=z["converged"], failed_at=z["failed_at"])
+    ocfg = oc.OracleConfig(max_iter=meta["max_iter"] or 0, **meta["params"])
     rep = compare(ref, got, z["y"], load_traces(z["traces"]) if greedy else None,
-                  got.get("trace"), algo)
+                  got.get("trace"), algo, replay=make_replay(algo, basis, z["y"], z["masks"], ocfg))
     print(json.dumps({k: v for k, v in rep.items() if k != "bad"}, default=str)[:400])
     assert not rep["bad"], rep
     assert len(rep["ties"]) <= 2, rep
@@ -115,7 +124,8 @@ def test_gpu_matches_oracle(cube, algo, params, cap, npix):
     ocfg = oc.OracleConfig(max_iter=cap or 0, **params)
     ref = oc.solve_cube(algo, c.basis, c.y, c.masks, ocfg, jobs=8, trace=greedy)
     refd = dict(x=ref.x, iterations=ref.iterations, converged=ref.converged, failed_at=ref.failed_at)
-    rep = compare(refd, got, c.y, ref.traces, got.get("trace"), algo)
+    rep = compare(refd, got, c.y, ref.traces, got.get("trace"), algo,
+                  replay=make_replay(algo, c.basis, c.y, c.masks, ocfg))
     print(json.dumps({k: (v if k != "ties" else v[:5]) for k, v in rep.items() if k != "bad"}, default=str)[:600])
     assert not rep["bad"], rep["bad"][:5]
     assert len(rep["ties"]) <= max(2, int(0.02 * npix)), rep["ties"][:5]
@@ -157,6 +167,7 @@ def test_cosamp_cycling_tail_pixels():
                         chunk=1, trace=True)
     assert (ref.iterations[:10] == 2000).all() and not ref.converged[:10].any()
     refd = dict(x=ref.x, iterations=ref.iterations, converged=ref.converged, failed_at=ref.failed_at)
-    rep = compare(refd, got, y, ref.traces, got.get("trace"), "cosamp")
+    rep = compare(refd, got, y, ref.traces, got.get("trace"), "cosamp",
+                  replay=make_replay("cosamp", c.basis, y, masks, oc.OracleConfig(kappa=27, max_iter=2000)))
     assert not rep["bad"], rep["bad"]
     np.testing.assert_allclose(got["final_delta"], ref.final_delta, rtol=1e-6, atol=1e-12)

@@ -143,6 +143,16 @@ class TestComparator:
         rep = compare(ref, cand, y, tr_ref, tr_cand)
         assert len(rep["bad"]) == 1
 
+    def test_forced_selection_replay(self):
+        from oracle import cpu_solvers as oc
+        v = np.array([1.0, 1e-20, 2e-20, 0.5])
+        rec = oc.Recorder(force={0: (0, 1)}, ynorm=1.0)
+        # k = 2: the 2nd/3rd magnitudes (0.5 vs 2e-20) are well separated: not forced
+        assert tuple(oc.argmax_k(v, 2, rec)) == (0, 3) and rec.forced == 0
+        rec = oc.Recorder(force={0: (2,)}, ynorm=1e13)
+        # k = 1 with ||y|| = 1e13: max|v| = 1 <= 1e-12 * 1e13 is degenerate: forced
+        assert tuple(oc.argmax_k(v, 1, rec)) == (2,) and rec.forced == 1
+
     def test_helpers(self):
         assert first_divergence([[1, [0]]], [(1, (0,))]) is None
         assert first_divergence([[1, [0]], [1, [2]]], [(1, (0,)), (1, (3,))]) == 1

@@ -13,7 +13,7 @@ from oracle import cpu_solvers as oc  # noqa: E402
 from paper_2401_14762_b200 import synth  # noqa: E402
 from paper_2401_14762_b200.solvers import SolverConfig, solve_batch  # noqa: E402
 from parity import compare  # noqa: E402
-from test_gpu_parity import decode_trace  # noqa: E402
+from test_gpu_parity import decode_trace, make_replay  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cube", default="salinas")
@@ -37,10 +37,11 @@ if greedy:
     got["trace"] = decode_trace((b.trace, b.trace_len), n)
 ref = oc.solve_cube(args.algo, c.basis, c.y, c.masks, oc.OracleConfig(max_iter=cfg.max_iter or 0, **params),
                     jobs=16, trace=greedy)
+ocfg = oc.OracleConfig(max_iter=cfg.max_iter or 0, **params)
 rep = compare(dict(x=ref.x, iterations=ref.iterations, converged=ref.converged, failed_at=ref.failed_at), got, c.y,
-              ref.traces, got.get("trace"), args.algo)
+              ref.traces, got.get("trace"), args.algo, replay=make_replay(args.algo, c.basis, c.y, c.masks, ocfg))
 it_diff = int((ref.iterations != got["iterations"]).sum())
 print(json.dumps({"algo": args.algo, "kappa": args.kappa, "pixels": c.n_pixels, "bad": len(rep["bad"]),
-                  "ties": len(rep["ties"]), "iteration_mismatches": it_diff, "worst_rel": rep["worst_rel"],
+                  "ties": len(rep["ties"]), "ties_replay_ok": sum(1 for t in rep["ties"] if t.get("replay_ok")), "iteration_mismatches": it_diff, "worst_rel": rep["worst_rel"],
                   "iters_gpu": int(got["iterations"].sum()), "iters_oracle": int(ref.iterations.sum()),
                   "bad_examples": rep["bad"][:3], "tie_examples": rep["ties"][:3]}, default=str))
