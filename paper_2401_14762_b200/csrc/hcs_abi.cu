@@ -5,6 +5,7 @@
 // solvers.py:259-260, 306-307, 355-358 and the shape checks of :464-471 are
 // repeated here so a C caller gets HCS_EINVAL for the same inputs).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -133,6 +134,10 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   const int kalloc = hcs::greedy_kalloc_host(algo, M, prm->kappa, kGreedySmemCap);
   const size_t smem = hcs::greedy_smem_bytes(M, kalloc);
   int per_sm = hcs::greedy_blocks_per_sm(algo, M, smem);
+  if (const char* ov = getenv("HCS_GREEDY_PER_SM")) {   // diagnostics override
+    const int v = atoi(ov);
+    if (v >= 1 && v < per_sm) per_sm = v;
+  }
   if (per_sm < 1) per_sm = 1;
   if (per_sm > kMaxGreedyPerSm) per_sm = kMaxGreedyPerSm;
   long long grid = (long long)sms * per_sm;

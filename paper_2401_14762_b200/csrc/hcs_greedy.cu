@@ -31,13 +31,12 @@ __device__ unsigned long long g_phase[16];
 #endif
 
 constexpr int kGreedyThreads = 128;
-constexpr int kRing = 32;  // state hashes kept for cycle detection (periods 2..31)
+constexpr int kRing = 64;  // state hashes kept for cycle detection (periods 2..63)
 
 struct GreedyShared {
   uint32_t supp[8], sel[8], keep[8];
   double red[16];
-  uint32_t ringbm[kRing][8];
-  unsigned long long ringh[kRing];
+  unsigned long long ringh[kRing];   // hash of (residual bits, support bitmap) per pass
   uint32_t snapbm[8];
   unsigned long long hpart[4];
   long long pid;
@@ -58,7 +57,8 @@ struct GreedyShared {
 struct GreedyLayout {
   int Mp, bmax, gmax;        // padded rows; doubles for B and for the Gram tiles
   int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring, dinv, cv;   // double offsets
-  int ints;                  // int region offset (in doubles)
+  int ints;                  // pivoted-fallback perm (ints) offset, in doubles
+  int lists;                 // uint8 support lists + mask bytes offset, in doubles
   size_t bytes;
 };
 
@@ -74,8 +74,14 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   GreedyLayout L;
   L.Mp = (M + 7) & ~7;
   L.bmax = ls_doubles(M, kalloc);
-  if (L.bmax < 4 * kMaxN) L.bmax = 4 * kMaxN;     // also the correlation / residual scratch
+  if (L.bmax < 4 * kMaxN) L.bmax = 4 * kMaxN;     // also the correlation / residual / top-k key scratch
   L.gmax = csne_gram_doubles(kalloc);
+  if (L.gmax < 4 * (M + 2)) L.gmax = 4 * (M + 2);  // also the pivoted fallback's vn1, vn2, z, perm
+  L.keys = 0;                   // aliases the LS region (free outside solve())
+  L.vn1 = L.bmax;               // vn1 / vn2 / zt / perm alias the Gram region (free outside the
+  L.vn2 = L.vn1 + M + 2;        // CSNE solve; zt is also the CoSaMP prune buffer after it)
+  L.zt = L.vn2 + M + 2;
+  const int perm = L.zt + M + 2;
   int o = L.bmax + L.gmax;
   L.vec = o; o += kMaxN;
   L.x = o; o += kMaxN;
@@ -83,17 +89,13 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   L.r = o; o += M;
   L.yv = o; o += L.Mp;
   L.sv = o; o += M + 2;
-  L.vn1 = o; o += M + 2;
-  L.vn2 = o; o += M + 2;
-  L.zt = o; o += M + 2;
   L.dinv = o; o += M + 9;
   L.cv = o; o += M + 9;
-  o = (o + 1) & ~1;             // 16-byte alignment for the paired key loads
-  L.keys = o; o += kMaxN;
   L.ring = o; o += M;           // residual snapshot for exact cycle confirmation
-  L.ints = o;
-  // ints: perm (M + 2), list (256), tlist (256); then msk bytes, then GreedyShared
-  size_t b = sizeof(double) * (size_t)o + sizeof(int) * (size_t)(M + 2 + 2 * kMaxN) + (size_t)M;
+  L.ints = perm;
+  // lists (2 x 256 uint8), msk (M bytes), then GreedyShared
+  L.lists = o;
+  size_t b = sizeof(double) * (size_t)o + 2 * kMaxN + (size_t)M;
   b = (b + 15) & ~(size_t)15;
   b += sizeof(GreedyShared);
   L.bytes = (b + 15) & ~(size_t)15;
@@ -111,14 +113,14 @@ __host__ __device__ inline int greedy_kalloc(int algo, int M, int kappa) {
 }
 
 // Sorted index list of a 256-bit bitmap (one warp); returns the count.
-__device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, int* list) {
+__device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, uint8_t* list) {
   const int lane = threadIdx.x & 31;
   int base = 0;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const uint32_t word = bm[e];
     const bool on = (word >> lane) & 1u;
-    if (on) list[base + __popc(word & ((1u << lane) - 1u))] = 32 * e + lane;
+    if (on) list[base + __popc(word & ((1u << lane) - 1u))] = (uint8_t)(32 * e + lane);
     base += __popc(word);
   }
   __syncwarp();
@@ -142,9 +144,9 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
   double* yv = S + L.yv;        // Mp: blocked rhs
   double* sv = S + L.sv;        // LS solution
   int* perm = reinterpret_cast<int*>(S + L.ints);
-  int* list = perm + M + 2;     // sorted support
-  int* tlist = list + kMaxN;    // support of the new iterate
-  uint8_t* msk = reinterpret_cast<uint8_t*>(tlist + kMaxN);
+  uint8_t* list = reinterpret_cast<uint8_t*>(S + L.lists);   // sorted support
+  uint8_t* tlist = list + kMaxN;                             // support of the new iterate
+  uint8_t* msk = tlist + kMaxN;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(S + L.keys);
   double* snap = S + L.ring;    // residual snapshot (cycle confirmation)
   GreedyShared& g = *reinterpret_cast<GreedyShared*>(reinterpret_cast<uintptr_t>(msk + M + 15) & ~uintptr_t(15));
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
 
   // least squares on the dictionary columns `cols[0..K)` (+ y): blocked DMMA
   // Householder, exact pivoted restatement when the rank guard trips
-  auto solve = [&](const int* cols, int K) {
+  auto solve = [&](const uint8_t* cols, int K) {
     const bool shared_b = K <= kalloc;
     double* B = shared_b ? S : Bglob;
     const int ldb = csne_ld(M);                  // column-major; y is column K
@@ -412,6 +414,8 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
         if (lane == 0) g.hpart[warp] = h;
         mis = __syncthreads_or(mis);
         h = g.hpart[0] + g.hpart[1] + g.hpart[2] + g.hpart[3];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) h = (h ^ g.supp[e]) * 0x100000001B3ull;   // support bitmap (FNV-style)
         int per = 0;
         if (pend_p && iters == pend_t + pend_p) {
           // exact confirmation: the state recurred bit for bit after pend_p passes
@@ -424,10 +428,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
           const int hist = iters - 1 < kRing - 1 ? iters - 1 : kRing - 1;
           for (int pp = 2; pp <= hist && !pend_p; ++pp) {
             const int slot = (iters - pp) % kRing;
-            if (g.ringh[slot] != h) continue;
-            bool same = true;
-            for (int e = 0; e < 8; ++e) same &= g.ringbm[slot][e] == g.supp[e];
-            if (same) { pend_p = pp; pend_t = iters; }
+            if (g.ringh[slot] == h) { pend_p = pp; pend_t = iters; }
           }
           if (pend_p) {
             for (int j = tid; j < M; j += nt) snap[j] = r[j];
@@ -437,7 +438,6 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
         __syncthreads();
         if (tid == 0) {
           g.ringh[iters % kRing] = h;
-          for (int e = 0; e < 8; ++e) g.ringbm[iters % kRing][e] = g.supp[e];
         }
         if (per) {
           iters += ((a.prm.max_iter - iters) / per) * per;
@@ -468,8 +468,13 @@ __global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a)
 size_t greedy_smem_bytes(int M, int kalloc) { return greedy_layout(M, kalloc).bytes; }
 
 int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
+  // Shared-memory LS capacity: the solver's bound (greedy_kalloc), trimmed so
+  // that at least two CTAs fit on an SM (228 KB, 1 KB reserved per CTA);
+  // systems wider than that spill to the CTA's global scratch.
+  const size_t two_per_sm = 113 * 1024;
+  const size_t cap = smem_cap < two_per_sm ? smem_cap : two_per_sm;
   int k = greedy_kalloc(algo, M, kappa);
-  while (k > 8 && greedy_layout(M, k).bytes > smem_cap) k -= 8;
+  while (k > 8 && greedy_layout(M, k).bytes > cap) --k;
   return k;
 }
 
@@ -521,4 +526,15 @@ extern "C" int hcs_debug_phases(unsigned long long* out16, int reset) {
   (void)reset;
   return 1;
 #endif
+}
+
+// diagnostics: shared-memory LS capacity, dynamic shared bytes and CTAs per SM
+// the greedy kernel would use for (algo, M, kappa)
+extern "C" int hcs_debug_greedy_config(int algo, int M, int kappa, long long* out3) {
+  const int k = hcs::greedy_kalloc_host(algo, M, kappa, 200 * 1024);
+  const size_t smem = hcs::greedy_smem_bytes(M, k);
+  out3[0] = k;
+  out3[1] = (long long)smem;
+  out3[2] = hcs::greedy_blocks_per_sm(algo, M, smem);
+  return 0;
 }
