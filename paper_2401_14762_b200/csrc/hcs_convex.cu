@@ -32,6 +32,10 @@ namespace hcs {
 
 enum { kEmpty = 0, kActive = 1, kRetire = 2 };
 
+#ifdef HCS_PHASES
+__device__ unsigned long long g_phase_cx[16];
+#endif
+
 struct SlotState {
   long long pid[kSlots];
   long long rpid[kSlots];
@@ -194,6 +198,13 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
   __syncthreads();
 
   double acc[2][4][2];
+#ifdef HCS_PHASES
+  long long cph[16] = {0};
+  cph[15] = clock64();
+#define CMARK(k) HCS_MARKP(cph, k)
+#else
+#define CMARK(k) do {} while (0)
+#endif
   for (;;) {
     // ---- writeback of retiring slots (element layout) ---------------------
 #pragma unroll
@@ -229,6 +240,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     }
     if (threadIdx.x == 0) ss.n_active = 0;
     __syncthreads();
+    CMARK(0);
 
     // ---- per-slot phase R: refill, momentum weights, GEMM input (fista) ----
     for (int s = w; s < kSlots; s += W) {
@@ -260,12 +272,14 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
       }
     }
     __syncthreads();
+    CMARK(1);
     if (ss.n_active == 0) break;
 
     if (ALGO == kFista) {
       // ---- GEMM A: grad = Psi^T g; epilogue: prox-gradient + momentum -----
       tile_gemm(a.fragT, In, KS, acc);
       __syncthreads();
+      CMARK(2);
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
@@ -287,9 +301,11 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           if (bad) ss.flag[s] = 1;
         }
       __syncthreads();
+      CMARK(3);
       // ---- GEMM B: F = Psi x_new; epilogue: stage F for the residual -----
       tile_gemm(a.fragS, In, KS, acc);
       __syncthreads();
+      CMARK(4);
 #pragma unroll
       for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
@@ -297,6 +313,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) In[in_idx(acc_row(w, rb, lane), acc_col(cb, i, lane))] = acc[rb][cb][i];
       __syncthreads();
+      CMARK(5);
       // ---- per-slot phase S: residual, delta, stop rule (solvers.py:192-196)
       for (int s = w; s < kSlots; s += W) {
         if (ss.status[s] != kActive) continue;
@@ -316,10 +333,12 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
         }
       }
       __syncthreads();
+      CMARK(6);
     } else {
       // ---- GEMM S: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha)
       tile_gemm(a.fragS, In, KS, acc);
       __syncthreads();
+      CMARK(2);
       const double alpha = a.prm.alpha;
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
@@ -337,8 +356,10 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           }
         }
       __syncthreads();
+      CMARK(3);
       // ---- GEMM C: x = Psi^T u'; epilogue: shrink, dual update, gap --------
       tile_gemm(a.fragT, In, KS, acc);
+      CMARK(4);
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
@@ -366,6 +387,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           if (bad) ss.flag[s] = 1;
         }
       __syncthreads();
+    CMARK(5);
       // ---- per-slot phase S: residual from u' (A x = u'[mask]), stop rule ----
       for (int s = w; s < kSlots; s += W) {
         if (ss.status[s] != kActive) continue;
@@ -380,8 +402,13 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
         if (lane == 0) finish_iteration(a, ss, s, sqrt(d2), true);
       }
       __syncthreads();
+    CMARK(6);
     }
   }
+#ifdef HCS_PHASES
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 15; ++k) atomicAdd(&g_phase_cx[k], (unsigned long long)cph[k]);
+#endif
 }
 
 // Fragment-order copies of Psi and Psi^T, and u0 = Psi * (1/sqrt(N)) 1.
@@ -440,3 +467,19 @@ cudaError_t launch_convex(int algo, const ConvexArgs& args, int grid, cudaStream
 }
 
 }  // namespace hcs
+
+// debug builds: per-phase cycle totals of the convex kernel (summed over CTAs)
+extern "C" int hcs_debug_phases_cx(unsigned long long* out16, int reset) {
+#ifdef HCS_PHASES
+  cudaMemcpyFromSymbol(out16, hcs::g_phase_cx, 16 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(hcs::g_phase_cx, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out16;
+  (void)reset;
+  return 1;
+#endif
+}

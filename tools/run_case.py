@@ -40,7 +40,9 @@ def main():
     from paper_2401_14762_b200 import _native
     lib = _native.load()
     ph = (ctypes.c_ulonglong * 16)()
-    has_ph = hasattr(lib, "hcs_debug_phases") and lib.hcs_debug_phases(ph, 1) == 0
+    convex = args.algo in ("fista", "admm")
+    dbg = lib.hcs_debug_phases_cx if convex else lib.hcs_debug_phases
+    has_ph = dbg(ph, 1) == 0
     out = None
     for _ in range(args.reps):
         torch.cuda.synchronize()
@@ -52,10 +54,11 @@ def main():
         print(f"{args.algo} k={args.kappa} P={cube.n_pixels}: {dt * 1e3:.2f} ms, {cube.n_pixels / dt:.0f} px/s, "
               f"iters mean {it.mean():.2f} max {it.max()} total {it.sum()}, {dt / max(it.sum(), 1) * 1e6:.2f} us/iter")
         if has_ph:
-            lib.hcs_debug_phases(ph, 1)
-            names = ["stop", "corr", "select", "gather", "panel", "trail", "backsub", "post", "resid", "fallback",
-                     "result"]
-            tot = sum(ph[:11])
+            dbg(ph, 1)
+            names = (["writeback", "phaseR", "gemm1", "epi1", "gemm2", "epi2", "phaseS"] if convex else
+                     ["stop", "corr", "select", "gather", "gram", "chol", "solve", "post", "resid", "fallback",
+                      "result"])
+            tot = sum(ph[:len(names)])
             print("  phases (% of CTA cycles): " + ", ".join(f"{nm} {100.0 * ph[i] / max(tot, 1):.1f}"
                                                            for i, nm in enumerate(names)))
 
