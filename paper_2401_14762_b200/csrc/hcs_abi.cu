@@ -54,18 +54,20 @@ int hcs_abi_version(void) { return 100; }
 const char* hcs_last_error(void) { return g_err.c_str(); }
 
 size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
-  (void)P;
   size_t b = kHeader;
   if (algo == HCS_FISTA || algo == HCS_ADMM) {
     const int Np = pad16(N);
     b += 2 * align256(sizeof(double) * (size_t)Np * Np);   // fragS, fragT
     b += align256(sizeof(double) * (size_t)Np);            // u0
+    if (algo == HCS_FISTA && P > 0) b += align256(sizeof(double) * (size_t)P);   // Lipschitz constants
   } else if (greedy(algo)) {
     // per-CTA global scratch for systems beyond the shared-memory region
     b += align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm);
   }
   return b;
 }
+
+constexpr int kSmemPerBlock = 227 * 1024;
 
 static int validate(int algo, int64_t P, int32_t N, int32_t M, const hcs_params* prm) {
   if (algo < HCS_FISTA || algo > HCS_COSAMP) return fail(HCS_EINVAL, "unknown algorithm");
@@ -119,12 +121,21 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
 
   if (algo == HCS_FISTA || algo == HCS_ADMM) {
     const int Np = pad16(N);
-    double2* fragS = reinterpret_cast<double2*>(ws + kHeader);
-    double2* fragT = reinterpret_cast<double2*>(ws + kHeader + align256(sizeof(double) * (size_t)Np * Np));
+    if (hcs::convex_smem_bytes(algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm, Np, M) > (size_t)kSmemPerBlock)
+      return fail(HCS_EINVAL, "convex solvers: 32 pixel slots of N = " + std::to_string(N) + ", M = " +
+                                  std::to_string(M) + " exceed the 227 KB shared memory of one SM");
+    double* fragS = reinterpret_cast<double*>(ws + kHeader);
+    double* fragT = reinterpret_cast<double*>(ws + kHeader + align256(sizeof(double) * (size_t)Np * Np));
     double* u0 = reinterpret_cast<double*>(ws + kHeader + 2 * align256(sizeof(double) * (size_t)Np * Np));
+    double* lip = reinterpret_cast<double*>(ws + kHeader + 2 * align256(sizeof(double) * (size_t)Np * Np) +
+                                            align256(sizeof(double) * (size_t)Np));
     e = hcs::launch_prep_basis(basis, N, Np, fragS, fragT, u0, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_basis_kernel");
-    hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, x_out, st, pr, counter, err};
+    if (algo == HCS_FISTA) {
+      e = hcs::launch_lipschitz_prepass(P, M, mask, u0, lip, sms, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "lipschitz_prepass_kernel");
+    }
+    hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, lip, x_out, st, pr, counter, err};
     const long long tiles = (P + hcs::kSlots - 1) / hcs::kSlots;
     const int grid = (int)(tiles < sms ? tiles : sms);
     e = hcs::launch_convex(algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm, args, grid, stream);

@@ -30,7 +30,7 @@
 
 namespace hcs {
 
-enum { kEmpty = 0, kActive = 1, kRetire = 2 };
+enum { kEmpty = 0, kActive = 1 };
 
 #ifdef HCS_PHASES
 __device__ unsigned long long g_phase_cx[16];
@@ -40,50 +40,90 @@ struct SlotState {
   long long pid[kSlots];
   long long rpid[kSlots];
   long long start[kSlots];
-  double delta[kSlots], t[kSlots], tn[kSlots], beta[kSlots], betan[kSlots];
-  double inv_l[kSlots], thr[kSlots], gap2[kSlots];
-  int status[kSlots], iter[kSlots], flag[kSlots], rfail[kSlots];
-  int n_active;
+  long long npid[kSlots];     // staged next pixel of the slot (>= P: none)
+  double slip[kSlots];        // its Lipschitz constant (fista)
+  double t[kSlots], tn[kSlots], betan[kSlots];
+  double inv_l[kSlots], thr[kSlots];
+  int status[kSlots], iter[kSlots], flag[kSlots], rfail[kSlots], retired[kSlots], moff[kSlots], need_pf[kSlots];
+  int nact[2];
   int exhausted;
 };
 
-// Pull pixels from the work queue into slot s until one needs iterating
-// (zero pixels retire on the spot, solvers.py:169-170 / 212-213).
+__host__ __device__ __forceinline__ int stage_mask_bytes(int M) { return ((M + 7) & ~7) + 8; }
+
+// Claim the slot's next pixel from the work queue and start copying its
+// measurements, mask row and (fista) Lipschitz constant into the slot's
+// staging area with cp.async: the refill that consumes it, usually many ticks
+// later, finds the data in shared memory instead of waiting on HBM.  Called
+// by the owning warp (cp.async completion is per thread).
 template <int ALGO>
-__device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, double* r, double* rp,
-                            uint8_t* msk, uint8_t* pos, int s) {
+__device__ void prefetch_slot(const ConvexArgs& a, SlotState& ss, double* sy, uint8_t* sm, int s) {
   const int lane = threadIdx.x & 31;
-  const int M = a.M, N = a.N;
+  const int M = a.M, Mm = stage_mask_bytes(M);
+  long long pid = 0;
+  if (lane == 0) {
+    pid = ss.exhausted ? a.P : (long long)atomicAdd(a.counter, 1ull);
+    if (pid >= a.P) ss.exhausted = 1;
+    ss.npid[s] = pid;
+  }
+  pid = __shfl_sync(0xffffffffu, pid, 0);
+  if (pid >= a.P) return;
+  for (int j = lane; j < M; j += 32) cp_async8(sy + s * M + j, a.y + pid * M + j);
+  // mask row: the 8-byte aligned chunks covering it (plain loads when the
+  // chunks would leave the array or the base is misaligned)
+  const unsigned long long b0 = (unsigned long long)pid * M, a0 = b0 & ~7ull;
+  int moff = (int)(b0 - a0);
+  const int nch = (moff + M + 7) >> 3;
+  if ((reinterpret_cast<uintptr_t>(a.mask) & 7) == 0 && a0 + 8ull * nch <= (unsigned long long)a.P * M) {
+    for (int c = lane; c < nch; c += 32) cp_async8b(sm + s * Mm + 8 * c, a.mask + a0 + 8 * c);
+  } else {
+    for (int j = lane; j < M; j += 32) sm[s * Mm + j] = a.mask[b0 + j];
+    moff = 0;
+  }
+  if (lane == 0) {
+    if (ALGO == kFista) cp_async8(&ss.slip[s], a.lip + pid);
+    ss.moff[s] = moff;
+  }
+}
+
+// Take the slot's staged pixel (zero pixels retire on the spot,
+// solvers.py:169-170 / 212-213) and set the slot up: measurements, residual
+// r = y, the row -> measurement map pos, and the slot's column of the first
+// GEMM's input (fista: g = A z - y = -y at the measured rows; admm: z - w = 0);
+// the next pixel is staged right after the slot phase (need_pf), where the
+// queue atomic's round trip overlaps the other warps' GEMM work.  Called by
+// the owning warp.
+template <int ALGO>
+__device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, double* bufB, double* ys, double* r,
+                            uint8_t* pos, double* sy, uint8_t* sm, int s) {
+  const int lane = threadIdx.x & 31;
+  const int M = a.M, N = a.N, Np = a.Np, Mm = stage_mask_bytes(M);
+  uint8_t* ps = pos + s * kMaxN;
+  for (int n = lane; n < Np; n += 32) {
+    bufA[in_idx(n, s)] = 0.0;
+    if (ALGO == kFista) bufB[in_idx(n, s)] = 0.0;   // z_0 = 0
+  }
   for (;;) {
-    long long pid = 0;
-    if (lane == 0) {
-      pid = ss.exhausted ? a.P : (long long)atomicAdd(a.counter, 1ull);
-      if (pid >= a.P) ss.exhausted = 1;
-    }
-    pid = __shfl_sync(0xffffffffu, pid, 0);
+    cp_async_wait_all();
+    __syncwarp();
+    const long long pid = ss.npid[s];
     if (pid >= a.P) {
       if (lane == 0) ss.status[s] = kEmpty;
-      if (ALGO == kAdmm)
-        for (int b = lane; b < kMaxN; b += 32) pos[s * kMaxN + b] = 0xFF;
+      for (int b = lane; b < kMaxN; b += 32) ps[b] = 0xFF;
       __syncwarp();
       return;
     }
     bool nz = false, bad = false;
     for (int j = lane; j < M; j += 32) {
-      double v = a.y[pid * M + j];
-      uint8_t mj = a.mask[pid * M + j];
+      const double v = sy[s * M + j];
       ys[s * M + j] = v;
       r[s * M + j] = v;
-      if (ALGO == kFista) rp[s * M + j] = v;
-      msk[s * M + j] = mj;
       nz |= (v != 0.0);
       bad |= !isfinite(v);
     }
     nz = __any_sync(0xffffffffu, nz);
     bad = __any_sync(0xffffffffu, bad);
-    __syncwarp();
-    double lip = 0.0;
-    if (ALGO == kFista) lip = warp_lipschitz(a.u0, msk + s * M, M);
+    const double lip = (ALGO == kFista) ? ss.slip[s] : 0.0;
     if (lane == 0 && a.st.lipschitz) a.st.lipschitz[pid] = (ALGO == kFista) ? lip : __longlong_as_double(0x7ff8000000000000ll);
     if (!nz) {  // y == 0: x = 0, 0 iterations, converged, delta 0, no admm_gap
       for (int n = lane; n < N; n += 32) a.x_out[pid * N + n] = 0.0;
@@ -96,6 +136,8 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, doub
         if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
         if (a.st.work) a.st.work[pid] = 0.0;
       }
+      __syncwarp();
+      prefetch_slot<ALGO>(a, ss, sy, sm, s);
       continue;
     }
     if (ALGO == kAdmm && bad && lane == 0) atomicOr(a.err, 1);   // cho_solve would raise
@@ -113,21 +155,24 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, doub
         if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - t0);
         if (a.st.work) a.st.work[pid] = 0.0;
       }
+      __syncwarp();
+      prefetch_slot<ALGO>(a, ss, sy, sm, s);
       continue;
     }
-    if (ALGO == kAdmm) {
-      for (int b = lane; b < kMaxN; b += 32) pos[s * kMaxN + b] = 0xFF;
-      __syncwarp();
-      for (int j = lane; j < M; j += 32) pos[s * kMaxN + msk[s * M + j]] = (uint8_t)j;
+    for (int b = lane; b < kMaxN; b += 32) ps[b] = 0xFF;
+    __syncwarp();
+    const uint8_t* mrow = sm + s * Mm + ss.moff[s];
+    for (int j = lane; j < M; j += 32) {
+      const int row = mrow[j];
+      ps[row] = (uint8_t)j;
+      if (ALGO == kFista) bufA[in_idx(row, s)] = -ys[s * M + j];
     }
     if (lane == 0) {
       ss.pid[s] = pid;
       ss.start[s] = t0;
       ss.status[s] = kActive;
       ss.iter[s] = 0;
-      ss.delta[s] = 1.0;
       ss.t[s] = 1.0;
-      ss.beta[s] = 0.0;
       if (ALGO == kFista) {
         ss.inv_l[s] = 1.0 / lip;
         ss.thr[s] = __dmul_rn(a.prm.lam, ss.inv_l[s]);
@@ -135,25 +180,25 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* ys, doub
         ss.thr[s] = a.prm.lam / a.prm.alpha;
       }
     }
+    if (lane == 0) ss.need_pf[s] = 1;   // staged after the barrier, off the slot phase
     __syncwarp();
     return;
   }
 }
 
 // Stop rule after an iteration (solvers.py:115-127 evaluated before the next
-// pass) plus the non-finite check (solvers.py:155-157).
+// pass) plus the non-finite check (solvers.py:155-157).  Lane 0 of the owner.
 __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState& ss, int s, double delta,
-                                                 bool admm) {
-  // lane 0 only
+                                                 bool admm, double gap2) {
   int it = ss.iter[s] + 1;
   ss.iter[s] = it;
-  ss.delta[s] = delta;
   const bool failed = ss.flag[s] || !isfinite(delta);
   const int dec = failed ? kContinue : stop_decision(delta, it, ss.start[s], a.prm);
   const bool conv = dec == kConverged;
   if (failed || dec != kContinue) {
     long long pid = ss.pid[s];
-    ss.status[s] = kRetire;
+    ss.status[s] = kEmpty;
+    ss.retired[s] = 1;
     ss.rpid[s] = pid;
     ss.rfail[s] = failed;
     a.st.iterations[pid] = failed ? 0 : it;
@@ -161,29 +206,45 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState&
     a.st.final_delta[pid] = failed ? __longlong_as_double(0x7ff8000000000000ll) : delta;
     a.st.failed_at[pid] = failed ? it : -1;
     if (admm && a.st.admm_gap)
-      a.st.admm_gap[pid] = failed ? __longlong_as_double(0x7ff8000000000000ll) : sqrt(ss.gap2[s]);
+      a.st.admm_gap[pid] = failed ? __longlong_as_double(0x7ff8000000000000ll) : sqrt(gap2);
     if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - ss.start[s]);
     if (a.st.work) a.st.work[pid] = 4.0 * (double)a.N * (double)a.N * (double)it;
   }
 }
 
-// 13..16 warps put 4 warps on one SM sub-partition (16K registers): <= 128 regs
+// One tick = one solver iteration of all 32 slots:
+//   slot phase (stop rule on the partial sums, refill)                | barrier
+//   writeback of retired slots; GEMM 1 (reads A); epilogue 1 (writes B) | barrier
+//   GEMM 2 (reads B); epilogue 2 (writes A for the next tick)          | barrier
+// (admm: A = z - w, B = u'; each buffer is written only after every warp is
+// done reading it, so no barrier sits between a GEMM and its epilogue.
+// fista: A holds g, then x_{k+1}, then the next g, B holds z (registers are
+// full at 128), two more barriers.)  Per-element iterates stay in registers
+// in the accumulator layout: fista p0 = x_k; admm p1 = w (z goes to x_out
+// every pass).
+// Residual-delta and ADMM-gap sums are reduced per warp (col_reduce8) into
+// part[], summed in fixed order by the slot's owner: deterministic.
+// 13..16 warps put 4 warps on one SM sub-partition (16K registers): <= 128 regs.
 template <int ALGO, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int Np = a.Np, M = a.M, N = a.N, KS = Np >> 2;
   const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* In = reinterpret_cast<double*>(smraw);        // Np * 32, B-fragment order
-  double* zs = In + Np * kSlots;                        // Np * 32 (fista: extrapolated point z)
-  double* ys = zs + (ALGO == kFista ? Np * kSlots : 0); // 32 * M
+  int rb0, nrb;
+  warp_rows(Np >> 3, w, rb0, nrb);
+  const int row0 = 8 * rb0 + (lane >> 2);   // element row of acc[rb] is row0 + 8 rb
+  double* bufA = reinterpret_cast<double*>(smraw);      // Np * 32: fista g / x_{k+1}, admm z - w
+  double* bufB = bufA + Np * kSlots;                    // Np * 32: fista z, admm u'
+  double* ys = bufB + Np * kSlots;                      // 32 * M
   double* r = ys + kSlots * M;                          // 32 * M
-  double* rp = r + kSlots * M;                          // 32 * M (fista)
-  SlotState& ss = *reinterpret_cast<SlotState*>(rp + (ALGO == kFista ? kSlots * M : 0));
-  uint8_t* msk = reinterpret_cast<uint8_t*>(&ss + 1);   // 32 * M
-  uint8_t* pos = msk + kSlots * M;                      // 32 * 256 (admm)
+  double* partD = r + kSlots * M;                       // 16 * 32 residual-delta partials
+  double* partG = partD + 16 * kSlots;                  // 16 * 32 admm gap partials
+  double* sy = partG + 16 * kSlots;                     // 32 * M staged next measurements
+  SlotState& ss = *reinterpret_cast<SlotState*>(sy + kSlots * M);
+  uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // 32 * 256: row -> measurement index
+  uint8_t* sm = pos + kSlots * kMaxN;                   // 32 * stage_mask_bytes(M) staged mask rows
+  const int cred = col_of_reduced(lane);
 
-  // per-element iterates in the accumulator layout: fista x (z in shared
-  // memory, register budget is 128 at 13+ warps); admm z, w
   double p0[2][4][2], p1[2][4][2];
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb)
@@ -191,11 +252,22 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
       for (int i = 0; i < 2; ++i) p0[rb][cb][i] = p1[rb][cb][i] = 0.0;
-  if (ALGO == kFista)
-    for (int idx = threadIdx.x; idx < Np * kSlots; idx += blockDim.x) zs[idx] = 0.0;
-  if (threadIdx.x < kSlots) ss.status[threadIdx.x] = kEmpty;
-  if (threadIdx.x == 0) ss.exhausted = 0;
+  if (threadIdx.x < kSlots) {
+    ss.status[threadIdx.x] = kEmpty;
+    ss.retired[threadIdx.x] = 0;
+    ss.need_pf[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    ss.exhausted = 0;
+    ss.nact[0] = ss.nact[1] = 0;
+  }
   __syncthreads();
+  for (int s = w; s < kSlots; s += W) prefetch_slot<ALGO>(a, ss, sy, sm, s);
+  // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
+  const double* mat1 = (ALGO == kFista) ? a.fragT : a.fragS;
+  const double* mat2 = (ALGO == kFista) ? a.fragS : a.fragT;
+  double2 af[4];
+  gemm_preload(nrb, mat1, rb0, KS, af);
 
   double acc[2][4][2];
 #ifdef HCS_PHASES
@@ -205,79 +277,78 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
 #else
 #define CMARK(k) do {} while (0)
 #endif
-  for (;;) {
-    // ---- writeback of retiring slots (element layout) ---------------------
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int s = acc_col(cb, i, lane);
-        if (ss.status[s] == kRetire) {
-          const long long pid = ss.rpid[s];
-          const bool fail = ss.rfail[s];
-#pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
-            const int n = acc_row(w, rb, lane);
-            const double v = (ALGO == kFista) ? p0[rb][cb][i] : p0[rb][cb][i];
-            if (n < N) a.x_out[pid * N + n] = fail ? 0.0 : v;
-            p0[rb][cb][i] = 0.0;
-            p1[rb][cb][i] = 0.0;
-            if (ALGO == kFista) zs[in_idx(n, s)] = 0.0;
-          }
-        }
-      }
-    if (ALGO == kFista) {
-      for (int idx = threadIdx.x; idx < Np * kSlots; idx += blockDim.x) In[idx] = 0.0;
-    } else {
-      // q = z - w is the GEMM input of the next ADMM pass
-#pragma unroll
-      for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            In[in_idx(acc_row(w, rb, lane), acc_col(cb, i, lane))] = p0[rb][cb][i] - p1[rb][cb][i];
-    }
-    if (threadIdx.x == 0) ss.n_active = 0;
-    __syncthreads();
-    CMARK(0);
-
-    // ---- per-slot phase R: refill, momentum weights, GEMM input (fista) ----
+  for (int tick = 0;; ++tick) {
+    const int par = tick & 1;
+    // ---- slot phase: stop rule of the last iteration, refill, momentum ----
     for (int s = w; s < kSlots; s += W) {
-      if (ss.status[s] != kActive) refill_slot<ALGO>(a, ss, ys, r, rp, msk, pos, s);
+      if (lane == 0) ss.retired[s] = 0;
       if (ss.status[s] == kActive) {
+        double dd = lane < W ? partD[lane * kSlots + s] : 0.0;
+        double gg = (ALGO == kAdmm && lane < W) ? partG[lane * kSlots + s] : 0.0;
+        dd = warp_sum(dd);
+        if (ALGO == kAdmm) gg = warp_sum(gg);
         if (lane == 0) {
-          atomicAdd(&ss.n_active, 1);
+          if (ALGO == kFista) ss.t[s] = ss.tn[s];
+          finish_iteration(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
+        }
+        __syncwarp();
+        if (ALGO == kAdmm && ss.retired[s] && ss.rfail[s])   // NumericalFailure: x = 0
+          for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[s] * N + n] = 0.0;
+      }
+      if (ss.status[s] != kActive) refill_slot<ALGO>(a, ss, bufA, bufB, ys, r, pos, sy, sm, s);
+      if (lane == 0) {
+        if (ss.status[s] == kActive) {
+          atomicAdd(&ss.nact[par], 1);
           ss.flag[s] = 0;
-          ss.gap2[s] = 0.0;
           if (ALGO == kFista) {
             const double t = ss.t[s];
             const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));   // solvers.py:160-161
             ss.tn[s] = tn;
             ss.betan[s] = (t - 1.0) / tn;
           }
+        } else {
+          ss.inv_l[s] = 0.0;
+          ss.thr[s] = 0.0;
+          ss.betan[s] = 0.0;
         }
-        if (ALGO == kFista) {
-          // g = A z - y = -(1 + b) r + b r_prev at the measured rows
-          const double b = ss.beta[s];
-          for (int j = lane; j < M; j += 32) {
-            const double g = -(1.0 + b) * r[s * M + j] + b * rp[s * M + j];
-            In[in_idx(msk[s * M + j], s)] = (b == 0.0) ? -r[s * M + j] : g;
-          }
-        }
-      } else if (lane == 0) {
-        ss.inv_l[s] = 0.0;
-        ss.thr[s] = 0.0;
-        ss.betan[s] = 0.0;
       }
     }
+    if (threadIdx.x == 0) ss.nact[par ^ 1] = 0;
     __syncthreads();
-    CMARK(1);
-    if (ss.n_active == 0) break;
+    CMARK(0);
+    for (int s = w; s < kSlots; s += W)
+      if (ss.need_pf[s]) {
+        __syncwarp();
+        if (lane == 0) ss.need_pf[s] = 0;
+        prefetch_slot<ALGO>(a, ss, sy, sm, s);
+      }
 
+    // ---- writeback of retired slots (element layout), fresh iterates -------
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int s = acc_col(cb, i, lane);
+        if (ss.retired[s]) {
+          const long long pid = ss.rpid[s];
+          const bool fail = ss.rfail[s];
+#pragma unroll
+          for (int rb = 0; rb < 2; ++rb) {
+            if (rb >= nrb) break;
+            const int n = row0 + 8 * rb;
+            if (ALGO == kFista && n < N) a.x_out[pid * N + n] = fail ? 0.0 : p0[rb][cb][i];
+            p0[rb][cb][i] = 0.0;
+            p1[rb][cb][i] = 0.0;
+          }
+        }
+      }
+    if (ss.nact[par] == 0) break;
+    CMARK(1);
+
+    double part[8];
     if (ALGO == kFista) {
-      // ---- GEMM A: grad = Psi^T g; epilogue: prox-gradient + momentum -----
-      tile_gemm(a.fragT, In, KS, acc);
+      // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
+      tile_gemm(nrb, a.fragT, rb0, bufA, KS, acc, af);
       __syncthreads();
       CMARK(2);
 #pragma unroll
@@ -289,76 +360,93 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           bool bad = false;
 #pragma unroll
           for (int rb = 0; rb < 2; ++rb) {
-            const int zi = in_idx(acc_row(w, rb, lane), s);
-            const double x = p0[rb][cb][i], z = zs[zi];
+            if (rb >= nrb) break;
+            const int zi = in_idx(row0 + 8 * rb, s);
+            const double x = p0[rb][cb][i], z = bufB[zi];
             const double aux = __dsub_rn(z, __dmul_rn(il, acc[rb][cb][i]));   // solvers.py:183
             const double xn = soft(aux, th);                                    // solvers.py:185
-            zs[zi] = __dadd_rn(xn, __dmul_rn(bn, __dsub_rn(xn, x)));           // solvers.py:189
+            bufB[zi] = __dadd_rn(xn, __dmul_rn(bn, __dsub_rn(xn, x)));         // solvers.py:189
             p0[rb][cb][i] = xn;
             bad |= !isfinite(xn);
-            In[in_idx(acc_row(w, rb, lane), s)] = xn;
+            bufA[zi] = xn;
           }
           if (bad) ss.flag[s] = 1;
         }
+      gemm_preload(nrb, mat2, rb0, KS, af);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(3);
-      // ---- GEMM B: F = Psi x_new; epilogue: stage F for the residual -----
-      tile_gemm(a.fragS, In, KS, acc);
+      // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
+      tile_gemm(nrb, a.fragS, rb0, bufA, KS, acc, af);
       __syncthreads();
       CMARK(4);
-#pragma unroll
-      for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) In[in_idx(acc_row(w, rb, lane), acc_col(cb, i, lane))] = acc[rb][cb][i];
-      __syncthreads();
-      CMARK(5);
-      // ---- per-slot phase S: residual, delta, stop rule (solvers.py:192-196)
-      for (int s = w; s < kSlots; s += W) {
-        if (ss.status[s] != kActive) continue;
-        double d2 = 0.0;
-        for (int j = lane; j < M; j += 32) {
-          const double rn = ys[s * M + j] - In[in_idx(msk[s * M + j], s)];
-          const double d = rn - r[s * M + j];
-          d2 += d * d;
-          rp[s * M + j] = r[s * M + j];
-          r[s * M + j] = rn;
-        }
-        d2 = warp_sum(d2);
-        if (lane == 0) {
-          ss.t[s] = ss.tn[s];
-          ss.beta[s] = ss.betan[s];
-          finish_iteration(a, ss, s, sqrt(d2), false);
-        }
-      }
-      __syncthreads();
-      CMARK(6);
-    } else {
-      // ---- GEMM S: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha)
-      tile_gemm(a.fragS, In, KS, acc);
-      __syncthreads();
-      CMARK(2);
-      const double alpha = a.prm.alpha;
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
+          const double bn = ss.betan[s];
+          double dd = 0.0;
 #pragma unroll
           for (int rb = 0; rb < 2; ++rb) {
-            const int n = acc_row(w, rb, lane);
+            if (rb >= nrb) break;
+            const int n = row0 + 8 * rb;
             const int pj = pos[s * kMaxN + n];
-            const bool in_mask = pj != 0xFF && n < N;
-            const double yh = in_mask ? ys[s * M + pj] : 0.0;
-            const double u = yh + alpha * acc[rb][cb][i];
-            In[in_idx(n, s)] = u / ((in_mask ? 1.0 : 0.0) + alpha);
+            double g = 0.0;
+            if (pj != 0xFF) {   // measured row: r = y - A x (solvers.py:192-196)
+              const double rn = ys[s * M + pj] - acc[rb][cb][i];
+              const double ro = r[s * M + pj];
+              const double d = rn - ro;
+              dd += d * d;
+              r[s * M + pj] = rn;
+              // next gradient input A z - y = -(1 + b) r + b r_prev
+              g = (bn == 0.0) ? -rn : -(1.0 + bn) * rn + bn * ro;
+            }
+            bufA[in_idx(n, s)] = g;
           }
+          part[2 * cb + i] = dd;
         }
+      partD[w * kSlots + cred] = col_reduce8(part, lane);
+      gemm_preload(nrb, mat1, rb0, KS, af);   // next GEMM's first k-steps
+      __syncthreads();
+      CMARK(5);
+    } else {
+      // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
+      //      residual y - A x = y - u'[mask] of this iteration's x ----------
+      tile_gemm(nrb, a.fragS, rb0, bufA, KS, acc, af);
+      CMARK(2);
+      const double alpha = a.prm.alpha;
+      // 1 / (d + alpha) for d = 0, 1 (Psi orthonormal: the factor's eigenvalues)
+      const double inv0 = 1.0 / alpha, inv1 = 1.0 / (1.0 + alpha);
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int s = acc_col(cb, i, lane);
+          double dd = 0.0;
+#pragma unroll
+          for (int rb = 0; rb < 2; ++rb) {
+            if (rb >= nrb) break;
+            const int n = row0 + 8 * rb;
+            const int pj = pos[s * kMaxN + n];
+            const bool in_mask = pj != 0xFF;
+            const double yh = in_mask ? ys[s * M + pj] : 0.0;
+            const double up = (yh + alpha * acc[rb][cb][i]) * (in_mask ? inv1 : inv0);
+            bufB[in_idx(n, s)] = up;
+            if (in_mask) {
+              const double rn = yh - up;
+              const double d = rn - r[s * M + pj];
+              dd += d * d;
+              r[s * M + pj] = rn;
+            }
+          }
+          part[2 * cb + i] = dd;
+        }
+      partD[w * kSlots + cred] = col_reduce8(part, lane);
+      gemm_preload(nrb, mat2, rb0, KS, af);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(3);
-      // ---- GEMM C: x = Psi^T u'; epilogue: shrink, dual update, gap --------
-      tile_gemm(a.fragT, In, KS, acc);
+      // ---- GEMM 2: x = Psi^T u'; epilogue: shrink, dual update, gap --------
+      tile_gemm(nrb, a.fragT, rb0, bufB, KS, acc, af);
       CMARK(4);
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb)
@@ -366,43 +454,33 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
           const double th = ss.thr[s];
+          const bool act = ss.status[s] == kActive;
+          double* xo = a.x_out + ss.pid[s] * N;
           bool bad = false;
           double g2 = 0.0;
 #pragma unroll
           for (int rb = 0; rb < 2; ++rb) {
-            const double x = acc[rb][cb][i], z = p0[rb][cb][i], wv = p1[rb][cb][i];
-            (void)z;
+            if (rb >= nrb) break;
+            const int n = row0 + 8 * rb;
+            const double x = acc[rb][cb][i], wv = p1[rb][cb][i];
             const double zn = soft(__dadd_rn(x, wv), th);                 // solvers.py:229
-            p1[rb][cb][i] = __dsub_rn(__dadd_rn(wv, x), zn);              // solvers.py:231
-            p0[rb][cb][i] = zn;
+            const double wn = __dsub_rn(__dadd_rn(wv, x), zn);            // solvers.py:231
+            // z is the returned iterate: stored every pass (L2-absorbed), so
+            // it needs no registers between passes
+            if (act && n < N) xo[n] = zn;
+            p1[rb][cb][i] = wn;
+            bufA[in_idx(n, s)] = zn - wn;                                 // next GEMM 1 input
             const double dg = x - zn;
             g2 += dg * dg;
             bad |= !isfinite(zn);
           }
-          // sum the 8 row-lanes sharing this column, then one shared atomic
-          g2 += __shfl_xor_sync(0xffffffffu, g2, 4);
-          g2 += __shfl_xor_sync(0xffffffffu, g2, 8);
-          g2 += __shfl_xor_sync(0xffffffffu, g2, 16);
-          if (lane < 4) atomicAdd(&ss.gap2[s], g2);
+          part[2 * cb + i] = g2;
           if (bad) ss.flag[s] = 1;
         }
+      partG[w * kSlots + cred] = col_reduce8(part, lane);
+      gemm_preload(nrb, mat1, rb0, KS, af);   // next GEMM's first k-steps
       __syncthreads();
-    CMARK(5);
-      // ---- per-slot phase S: residual from u' (A x = u'[mask]), stop rule ----
-      for (int s = w; s < kSlots; s += W) {
-        if (ss.status[s] != kActive) continue;
-        double d2 = 0.0;
-        for (int j = lane; j < M; j += 32) {
-          const double rn = ys[s * M + j] - In[in_idx(msk[s * M + j], s)];
-          const double d = rn - r[s * M + j];
-          d2 += d * d;
-          r[s * M + j] = rn;
-        }
-        d2 = warp_sum(d2);
-        if (lane == 0) finish_iteration(a, ss, s, sqrt(d2), true);
-      }
-      __syncthreads();
-    CMARK(6);
+      CMARK(5);
     }
   }
 #ifdef HCS_PHASES
@@ -411,21 +489,26 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
 #endif
 }
 
-// Fragment-order copies of Psi and Psi^T, and u0 = Psi * (1/sqrt(N)) 1.
-__global__ void prep_basis_kernel(const double* __restrict__ basis, int N, int Np, double2* fragS,
-                                  double2* fragT, double* u0) {
-  const int KS = Np >> 2;
-  const long long total = (long long)(Np / 16) * KS * 32;
+// Fragment-order copies of Psi and Psi^T (layout of tile_gemm), and
+// u0 = Psi * (1/sqrt(N)) 1.  Row block rb's fragment for k-step ks, lane l is
+// Mat[8 rb + l/4][4 ks + l%4]; blocks owned in pairs by one warp (warp_rows)
+// are interleaved as double2.
+__global__ void prep_basis_kernel(const double* __restrict__ basis, int N, int Np, double* fragS, double* fragT,
+                                  double* u0) {
+  const int KS = Np >> 2, RB = Np >> 3;
+  const int nd = RB > 16 ? RB - 16 : 0;
+  const long long total = (long long)RB * KS * 32;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     const int lane = (int)(idx & 31);
     const long long t = idx >> 5;
     const int ks = (int)(t % KS);
-    const int w = (int)(t / KS);
-    const int r0 = 16 * w + (lane >> 2), r1 = r0 + 8, c = 4 * ks + (lane & 3);
-    auto at = [&](int rr, int cc) { return (rr < N && cc < N) ? basis[(size_t)rr * N + cc] : 0.0; };
-    fragS[idx] = make_double2(at(r0, c), at(r1, c));
-    fragT[idx] = make_double2(at(c, r0), at(c, r1));
+    const int rb = (int)(t / KS);
+    const int r = 8 * rb + (lane >> 2), c = 4 * ks + (lane & 3);
+    const size_t dst = rb < 2 * nd ? ((size_t)((rb >> 1) * KS + ks) * 32 + lane) * 2 + (rb & 1)
+                                   : ((size_t)rb * KS + ks) * 32 + lane;
+    fragS[dst] = (r < N && c < N) ? basis[(size_t)r * N + c] : 0.0;
+    fragT[dst] = (r < N && c < N) ? basis[(size_t)c * N + r] : 0.0;
   }
   if (blockIdx.x == 0) {
     const double inv = 1.0 / sqrt((double)N);
@@ -437,18 +520,40 @@ __global__ void prep_basis_kernel(const double* __restrict__ basis, int N, int N
   }
 }
 
-cudaError_t launch_prep_basis(const double* basis, int N, int Np, double2* fragS, double2* fragT, double* u0,
+// Lipschitz constants of every pixel's A (fista), one warp per pixel, ahead
+// of the slot engine so that a refill never waits on the power iteration.
+__global__ void lipschitz_prepass_kernel(long long P, int M, const uint8_t* __restrict__ mask,
+                                         const double* __restrict__ u0, double* __restrict__ lip) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long p = gw; p < P; p += nw) {
+    const double l = warp_lipschitz(u0, mask + p * M, M);
+    if (lane == 0) lip[p] = l;
+  }
+}
+
+cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
+                                     int sms, cudaStream_t stream) {
+  lipschitz_prepass_kernel<<<sms * 8, 256, 0, stream>>>(P, M, mask, u0, lip);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
                               cudaStream_t stream) {
   prep_basis_kernel<<<64, 256, 0, stream>>>(basis, N, Np, fragS, fragT, u0);
   return cudaGetLastError();
 }
 
 size_t convex_smem_bytes(int algo, int Np, int M) {
-  size_t b = sizeof(double) * (size_t)Np * kSlots * (algo == kFista ? 2 : 1);   // In (+ z)
-  b += sizeof(double) * (size_t)kSlots * M * (algo == kFista ? 3 : 2);
+  (void)algo;
+  size_t b = sizeof(double) * (size_t)Np * kSlots * 2;               // bufA, bufB
+  b += sizeof(double) * (size_t)kSlots * M * 2;                      // ys, r
+  b += sizeof(double) * 2 * 16 * kSlots;                             // partD, partG
+  b += sizeof(double) * (size_t)kSlots * M;                          // sy
   b += sizeof(SlotState);
-  b += (size_t)kSlots * M;                                           // msk
-  if (algo == kAdmm) b += (size_t)kSlots * kMaxN;                    // pos
+  b += (size_t)kSlots * kMaxN;                                       // pos
+  b += (size_t)kSlots * stage_mask_bytes(M);                         // sm
   return (b + 15) & ~(size_t)15;
 }
 
@@ -456,7 +561,7 @@ template <int ALGO, int MAXT>
 static cudaError_t launch_convex_t(const ConvexArgs& args, int grid, size_t smem, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  convex_kernel<ALGO, MAXT><<<grid, 2 * args.Np, smem, stream>>>(args);   // Np / 16 warps
+  convex_kernel<ALGO, MAXT><<<grid, 32 * engine_warps(args.Np), smem, stream>>>(args);
   return cudaGetLastError();
 }
 

@@ -5,12 +5,11 @@
 //     Out[n, s] = sum_k Mat[n, k] * In[k, s],   n, k < Np (N padded to 16)
 // where Mat is Psi or Psi^T (N x N, shared by every pixel, L2-resident) and
 // In is the CTA's 32 pixel vectors held in shared memory.  Warp w owns output
-// rows [16 w, 16 w + 16) for all 32 columns: 2 x 4 DMMA 8x8 accumulators.
+// one or two 8-row blocks for all 32 columns (warp_rows): up to 2 x 4 DMMA
+// 8x8 accumulators.
 //
 // Mat is pre-arranged once per call ("fragment order") so that each warp's A
-// fragments for one k-step are one coalesced 512-byte double2 load:
-//     frag[(w * KS + ks) * 32 + lane] = (Mat[16w + lane/4][4ks + lane%4],
-//                                        Mat[16w + 8 + lane/4][4ks + lane%4])
+// fragments for one k-step are one coalesced load (see tile_gemm).
 // In is stored in B-fragment order so the 4 B fragments of a k-step are
 // conflict-free 256-byte shared loads:  in_idx(k, s) below.
 #pragma once
@@ -30,44 +29,136 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// Element coordinates of accumulator acc[rb][cb][i] held by `lane` of warp w.
+// Element coordinates of accumulator acc[rb][cb][i] held by `lane` of warp w
+// (16-row warp tiles; used by the PSNR kernel).
 __device__ __forceinline__ int acc_row(int w, int rb, int lane) { return 16 * w + 8 * rb + (lane >> 2); }
 __device__ __forceinline__ int acc_col(int cb, int i, int lane) { return 8 * cb + 2 * (lane & 3) + i; }
 
-// acc = Mat(rows of warp w) * In.  KS = Np / 4 (a multiple of 4).
-__device__ __forceinline__ void tile_gemm(const double2* __restrict__ frag, const double* In, int KS,
-                                          double (&acc)[2][4][2]) {
+// Balanced row-block map of the slot engine.  RB = Np / 8 row blocks of 8
+// rows over min(RB, 16) warps: the first nd = RB - 16 warps own two blocks,
+// the rest one.  The DMMA pipe is per SM sub-partition (warp w runs on
+// sub-partition w % 4), so this spreads the blocks evenly: RB = 28 (N = 224)
+// puts exactly 7 blocks on every sub-partition, where 14 warps of 16 rows
+// would load two sub-partitions with 4 warps and two with 3 (87.5% cap).
+__device__ __forceinline__ void warp_rows(int RB, int w, int& rb0, int& nrb) {
+  const int nd = RB > 16 ? RB - 16 : 0;
+  if (w < nd) { rb0 = 2 * w; nrb = 2; } else { rb0 = nd + w; nrb = 1; }
+}
+__host__ __device__ __forceinline__ int engine_warps(int Np) { return (Np >> 3) < 16 ? (Np >> 3) : 16; }
+
+// A fragments of the first k-steps, loaded ahead of the GEMM (before the
+// barrier that precedes it) so that their L2 latency is off the critical path.
+// Two-block warps: a[i] = k-step i (both blocks); one-block warps:
+// a[i].x = k-step i, a[i].y = k-step i + 4.
+template <int NRB>
+__device__ __forceinline__ void gemm_preload(const double* __restrict__ frag, int rb0, int KS, double2 (&a)[4]) {
   const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const double2* fa = frag + (size_t)w * KS * 32 + lane;
+  if (NRB == 2) {
+    const double2* fa = reinterpret_cast<const double2*>(frag + (size_t)rb0 * KS * 32) + lane;
 #pragma unroll
-  for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
-  double2 a[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) a[i] = __ldg(fa + i * 32);
-  for (int ks0 = 0; ks0 < KS; ks0 += 4) {
-    double2 nxt[4];
-    const bool more = ks0 + 4 < KS;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) nxt[i] = more ? __ldg(fa + (ks0 + 4 + i) * 32) : a[i];
+    for (int i = 0; i < 4; ++i) a[i] = __ldg(fa + i * 32);
+  } else {
+    const double* fa = frag + (size_t)rb0 * KS * 32 + lane;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const double* b = In + ((ks0 + i) << 7) + lane;
-      double b0 = b[0], b1 = b[32], b2 = b[64], b3 = b[96];
-      dmma(acc[0][0], a[i].x, b0);
-      dmma(acc[1][0], a[i].y, b0);
-      dmma(acc[0][1], a[i].x, b1);
-      dmma(acc[1][1], a[i].y, b1);
-      dmma(acc[0][2], a[i].x, b2);
-      dmma(acc[1][2], a[i].y, b2);
-      dmma(acc[0][3], a[i].x, b3);
-      dmma(acc[1][3], a[i].y, b3);
+      a[i].x = __ldg(fa + i * 32);
+      a[i].y = 4 + i < KS ? __ldg(fa + (4 + i) * 32) : 0.0;
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = nxt[i];
   }
+}
+__device__ __forceinline__ void gemm_preload(int nrb, const double* frag, int rb0, int KS, double2 (&a)[4]) {
+  if (nrb == 2) gemm_preload<2>(frag, rb0, KS, a); else gemm_preload<1>(frag, rb0, KS, a);
+}
+
+// acc = Mat(row blocks rb0 .. rb0 + NRB - 1) * In.  KS = Np / 4 (a multiple of
+// 4).  frag is the fragment-order matrix of prep_basis_kernel: the A
+// fragments of row block rb start at double offset rb * KS * 32; a two-block
+// warp's pair is interleaved (one 16-byte load per lane and k-step).  a holds
+// the gemm_preload fragments on entry (consumed).
+template <int NRB>
+__device__ __forceinline__ void tile_gemm(const double* __restrict__ frag, int rb0, const double* In, int KS,
+                                          double (&acc)[2][4][2], double2 (&a)[4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+  if (NRB == 2) {
+    const double2* fa = reinterpret_cast<const double2*>(frag + (size_t)rb0 * KS * 32) + lane;
+    // a[i] is reloaded (4 k-steps ahead) right after its last use: prefetch
+    // distance 4 at 16 registers
+    for (int ks0 = 0; ks0 < KS; ks0 += 4) {
+      const bool more = ks0 + 4 < KS;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double* b = In + ((ks0 + i) << 7) + lane;
+        const double b0 = b[0], b1 = b[32], b2 = b[64], b3 = b[96];
+        dmma(acc[0][0], a[i].x, b0);
+        dmma(acc[1][0], a[i].y, b0);
+        dmma(acc[0][1], a[i].x, b1);
+        dmma(acc[1][1], a[i].y, b1);
+        dmma(acc[0][2], a[i].x, b2);
+        dmma(acc[1][2], a[i].y, b2);
+        dmma(acc[0][3], a[i].x, b3);
+        dmma(acc[1][3], a[i].y, b3);
+        if (more) a[i] = __ldg(fa + (ks0 + 4 + i) * 32);
+      }
+    }
+  } else {
+    const double* fa = frag + (size_t)rb0 * KS * 32 + lane;
+    // two 4-step halves: prefetch distance 8 k-steps (half the DMMAs per step)
+    for (int ks0 = 0; ks0 < KS; ks0 += 8) {
+      const bool more0 = ks0 + 8 < KS, more1 = ks0 + 12 < KS;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double* b = In + ((ks0 + i) << 7) + lane;
+        dmma(acc[0][0], a[i].x, b[0]);
+        dmma(acc[0][1], a[i].x, b[32]);
+        dmma(acc[0][2], a[i].x, b[64]);
+        dmma(acc[0][3], a[i].x, b[96]);
+        if (more0) a[i].x = __ldg(fa + (ks0 + 8 + i) * 32);
+      }
+      if (ks0 + 4 >= KS) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double* b = In + ((ks0 + 4 + i) << 7) + lane;
+        dmma(acc[0][0], a[i].y, b[0]);
+        dmma(acc[0][1], a[i].y, b[32]);
+        dmma(acc[0][2], a[i].y, b[64]);
+        dmma(acc[0][3], a[i].y, b[96]);
+        if (more1) a[i].y = __ldg(fa + (ks0 + 12 + i) * 32);
+      }
+    }
+  }
+}
+__device__ __forceinline__ void tile_gemm(int nrb, const double* frag, int rb0, const double* In, int KS,
+                                          double (&acc)[2][4][2], double2 (&a)[4]) {
+  if (nrb == 2) tile_gemm<2>(frag, rb0, In, KS, acc, a); else tile_gemm<1>(frag, rb0, In, KS, acc, a);
+}
+
+// Column sums of an accumulator-layout quantity: v[2 cb + i] is this lane's
+// value for slot column 8 cb + 2 (lane & 3) + i (already summed over its row
+// blocks).  Three transpose-and-add butterfly stages over the 8 lanes sharing
+// a column (lane bits 2..4) leave each lane with the full 8-row sum of one
+// column, col_of_reduced(lane): 7 double shuffles instead of 24.
+__device__ __forceinline__ double col_reduce8(const double (&v)[8], int lane) {
+  const bool b = (lane >> 2) & 1, c = (lane >> 3) & 1, e = (lane >> 4) & 1;
+  double u[4], q[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double send = b ? v[k] : v[k + 4], keep = b ? v[k + 4] : v[k];
+    u[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = c ? u[k] : u[k + 2], keep = c ? u[k + 2] : u[k];
+    q[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const double send = e ? q[0] : q[1], keep = e ? q[1] : q[0];
+  return keep + __shfl_xor_sync(0xffffffffu, send, 16);
+}
+__device__ __forceinline__ int col_of_reduced(int lane) {
+  return 8 * (2 * ((lane >> 2) & 1) + ((lane >> 3) & 1)) + 2 * (lane & 3) + ((lane >> 4) & 1);
 }
 
 }  // namespace hcs

@@ -12,9 +12,10 @@ struct ConvexArgs {
   int N, Np, M;
   const double* y;
   const uint8_t* mask;
-  const double2* fragT;   // Psi^T (analysis) in fragment order
-  const double2* fragS;   // Psi (synthesis) in fragment order
+  const double* fragT;    // Psi^T (analysis) in fragment order
+  const double* fragS;    // Psi (synthesis) in fragment order
   const double* u0;       // Psi * (1/sqrt(N)) 1, for the Lipschitz constant
+  double* lip;            // (P,) per-pixel Lipschitz constants (fista; lipschitz_prepass)
   double* x_out;
   Stats st;
   Params prm;
@@ -39,7 +40,9 @@ struct GreedyArgs {
 // hcs_convex.cu
 cudaError_t launch_convex(int algo, const ConvexArgs& args, int grid, cudaStream_t stream);
 size_t convex_smem_bytes(int algo, int Np, int M);
-cudaError_t launch_prep_basis(const double* basis, int N, int Np, double2* fragS, double2* fragT, double* u0,
+cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
+                                     int sms, cudaStream_t stream);
+cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
                               cudaStream_t stream);
 // hcs_greedy.cu
 cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream);

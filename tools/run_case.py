@@ -55,7 +55,7 @@ def main():
               f"iters mean {it.mean():.2f} max {it.max()} total {it.sum()}, {dt / max(it.sum(), 1) * 1e6:.2f} us/iter")
         if has_ph:
             dbg(ph, 1)
-            names = (["writeback", "phaseR", "gemm1", "epi1", "gemm2", "epi2", "phaseS"] if convex else
+            names = (["slots", "writeback", "gemm1", "epi1", "gemm2", "epi2"] if convex else
                      ["stop", "corr", "select", "gather", "gram", "chol", "solve", "post", "resid", "fallback",
                       "result"])
             tot = sum(ph[:len(names)])
