@@ -280,23 +280,36 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
   for (int tick = 0;; ++tick) {
     const int par = tick & 1;
     // ---- slot phase: stop rule of the last iteration, refill, momentum ----
-    for (int s = w; s < kSlots; s += W) {
-      if (lane == 0) ss.retired[s] = 0;
-      if (ss.status[s] == kActive) {
-        double dd = lane < W ? partD[lane * kSlots + s] : 0.0;
-        double gg = (ALGO == kAdmm && lane < W) ? partG[lane * kSlots + s] : 0.0;
-        dd = warp_sum(dd);
-        if (ALGO == kAdmm) gg = warp_sum(gg);
-        if (lane == 0) {
+    // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
+    // serial stop-rule / momentum code of a warp's slots runs side by side
+    for (int s0 = w; s0 < kSlots; s0 += 2 * W) {
+      const int hl = lane & 15, s = s0 + (lane >> 4) * W;
+      const bool valid = s < kSlots;
+      const bool was_active = valid && ss.status[s] == kActive;
+      double dd = (was_active && hl < W) ? partD[hl * kSlots + s] : 0.0;
+      double gg = (ALGO == kAdmm && was_active && hl < W) ? partG[hl * kSlots + s] : 0.0;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        dd += __shfl_xor_sync(0xffffffffu, dd, o);
+        if (ALGO == kAdmm) gg += __shfl_xor_sync(0xffffffffu, gg, o);
+      }
+      if (hl == 0 && valid) {
+        ss.retired[s] = 0;
+        if (was_active) {
           if (ALGO == kFista) ss.t[s] = ss.tn[s];
           finish_iteration(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
         }
-        __syncwarp();
-        if (ALGO == kAdmm && ss.retired[s] && ss.rfail[s])   // NumericalFailure: x = 0
-          for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[s] * N + n] = 0.0;
       }
-      if (ss.status[s] != kActive) refill_slot<ALGO>(a, ss, bufA, bufB, ys, r, pos, sy, sm, s);
-      if (lane == 0) {
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int sk = s0 + k * W;
+        if (sk >= kSlots) break;
+        if (ALGO == kAdmm && ss.retired[sk] && ss.rfail[sk])   // NumericalFailure: x = 0
+          for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
+        if (ss.status[sk] != kActive) refill_slot<ALGO>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+      }
+      if (hl == 0 && valid) {
         if (ss.status[s] == kActive) {
           atomicAdd(&ss.nact[par], 1);
           ss.flag[s] = 0;
@@ -312,6 +325,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           ss.betan[s] = 0.0;
         }
       }
+      __syncwarp();
     }
     if (threadIdx.x == 0) ss.nact[par ^ 1] = 0;
     __syncthreads();
