@@ -23,6 +23,7 @@
 #include "hcs_internal.cuh"
 #include "hcs_ls.cuh"
 #include "hcs_ls_csne.cuh"
+#include <cstdlib>
 
 namespace hcs {
 
@@ -128,7 +129,7 @@ __device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, uint8_t* list)
 }
 
 template <int ALGO>
-__global__ void __launch_bounds__(kGreedyThreads, 3) greedy_kernel(GreedyArgs a) {
+__global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int N = a.N, M = a.M;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -469,10 +470,18 @@ size_t greedy_smem_bytes(int M, int kalloc) { return greedy_layout(M, kalloc).by
 
 int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
   // Shared-memory LS capacity: the solver's bound (greedy_kalloc), trimmed so
-  // that at least two CTAs fit on an SM (228 KB, 1 KB reserved per CTA);
-  // systems wider than that spill to the CTA's global scratch.
-  const size_t two_per_sm = 113 * 1024;
-  const size_t cap = smem_cap < two_per_sm ? smem_cap : two_per_sm;
+  // that four CTAs fit on an SM (228 KB, 1 KB reserved per CTA; the register
+  // budget, launch bounds (128, 4), allows four too); systems wider than that
+  // spill to the CTA's global scratch.  The kernel is latency-bound (serial
+  // pivot chains, L2 gathers): four resident pixels per SM beat wider
+  // shared-memory systems at two or three (measured: BIHT k=33 1.7x, CoSaMP
+  // k=27 1.15x).
+  const size_t four_per_sm = 55 * 1024;
+  size_t cap = smem_cap < four_per_sm ? smem_cap : four_per_sm;
+  if (const char* ov = getenv("HCS_GREEDY_CAP_KB")) {   // experiments: tighter capacity, more CTAs per SM
+    const size_t v = (size_t)atoi(ov) * 1024;
+    if (v >= 16 * 1024 && v < cap) cap = v;
+  }
   int k = greedy_kalloc(algo, M, kappa);
   while (k > 8 && greedy_layout(M, k).bytes > cap) --k;
   return k;

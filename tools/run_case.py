@@ -57,7 +57,7 @@ def main():
             dbg(ph, 1)
             names = (["slots", "writeback", "gemm1", "epi1", "gemm2", "epi2"] if convex else
                      ["stop", "corr", "select", "gather", "gram", "chol", "solve", "post", "resid", "fallback",
-                      "result"])
+                      "result", "diag0", "panel", "trail"])
             tot = sum(ph[:len(names)])
             print("  phases (% of CTA cycles): " + ", ".join(f"{nm} {100.0 * ph[i] / max(tot, 1):.1f}"
                                                            for i, nm in enumerate(names)))
