@@ -174,23 +174,38 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
     const int nc = csne_cols(K);
     // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
     // copies columns w, w+4, ...; lanes over rows (consecutive shared words)
-    for (int c = warp; c < nc; c += 4) {
-      const int col = c < K ? cols[c] : 0;
-      for (int rr = lane; rr < ldb; rr += 32) {
-        double* dst = B + c * ldb + rr;
-        if (rr < M && c < K) {
-          const double* src = a.basis + (size_t)msk[rr] * N + col;
-          if (shared_b) cp_async8(dst, src);
-          else *dst = __ldg(src);
-        } else {
-          *dst = (rr < M && c == K) ? ys[rr] : 0.0;
+    if (shared_b) {
+      for (int c = warp; c < nc; c += 4) {
+        const int col = c < K ? cols[c] : 0;
+        for (int rr = lane; rr < ldb; rr += 32) {
+          double* dst = B + c * ldb + rr;
+          if (rr < M && c < K) cp_async8(dst, a.basis + (size_t)msk[rr] * N + col);
+          else *dst = (rr < M && c == K) ? ys[rr] : 0.0;
         }
       }
+      cp_async_wait_all();
+    } else {
+      // global scratch: eight independent loads in flight per thread
+      const int total = nc * ldb;
+      for (int i0 = tid; i0 < total; i0 += 8 * nt) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = i0 + u * nt, c = idx / ldb, rr = idx - c * ldb;
+          v[u] = 0.0;
+          if (idx < total && rr < M) v[u] = c < K ? __ldg(a.basis + (size_t)msk[rr] * N + cols[c]) : (c == K ? ys[rr] : 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * nt < total) B[i0 + u * nt] = v[u];
+      }
     }
-    cp_async_wait_all();
     __syncthreads();
     GMARK(3);
-    const CsneScratch cs{shared_b ? S + L.bmax : Gglob, S + L.dinv, S + L.cv, yv, g.red, lsflag};
+    // Gram tiles in shared memory whenever they fit the whole LS region (B then
+    // lives in the global scratch), else in the global scratch too
+    double* G = shared_b ? S + L.bmax : (csne_gram_doubles(K) <= L.bmax + L.gmax ? S : Gglob);
+    const CsneScratch cs{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
     if (ls_csne(B, ldb, M, K, sv, cs, php)) return;
     const int ldp = (K + 1) | 1;
     for (int idx = tid; idx < M * (K + 1); idx += nt) {
