@@ -562,3 +562,22 @@ extern "C" int hcs_debug_greedy_config(int algo, int M, int kappa, long long* ou
   out3[2] = hcs::greedy_blocks_per_sm(algo, M, smem);
   return 0;
 }
+
+// selection tests: cta_topk (variant 1) or the ranking reference (variant 0)
+// on `batch` vectors of length n (device pointers), one CTA each
+namespace hcs {
+__global__ void topk_test_kernel(const double* v, int n, int k, uint32_t* bm, int variant) {
+  __shared__ unsigned long long keys[256 + 16];
+  __shared__ uint32_t bmap[8];
+  const double* vv = v + (size_t)blockIdx.x * n;
+  if (variant) cta_topk(vv, n, k, bmap, keys);
+  else cta_topk_rank(vv, n, k, bmap, keys);
+  if (threadIdx.x < 8) bm[(size_t)blockIdx.x * 8 + threadIdx.x] = bmap[threadIdx.x];
+}
+}  // namespace hcs
+
+extern "C" int hcs_debug_cta_topk(const double* v, int batch, int n, int k, uint32_t* bm, int variant) {
+  if (n < 1 || n > 256 || k < 1 || k > n || batch < 1) return 1;
+  hcs::topk_test_kernel<<<batch, hcs::kGreedyThreads>>>(v, n, k, bm, variant);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 2;
+}
