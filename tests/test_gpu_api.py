@@ -272,3 +272,38 @@ class TestKernels:                                      # test_kernels.py
         assert hcs.residual_delta(np.array([1.0, 1.0]), np.array([0.0, 0.0])) == pytest.approx(math.sqrt(2.0))
         with pytest.raises(ValueError):
             hcs.residual_delta(np.ones(2), np.ones(3))
+
+
+@pytest.mark.parametrize("algo,params", [("fista", dict(lam=0.1)), ("admm", dict(lam=0.1, alpha=1.8)),
+                                         ("gomp", dict(kappa=22, atoms_per_iter=4)), ("cosamp", dict(kappa=22))])
+def test_chunked_host_pipeline_matches_one_launch(algo, params):
+    """recover_cube on host buffers pipelines pixel chunks over two compute
+    streams; results must equal the single device launch bit for bit."""
+    c = synth.generate(6, 10, 154, seed=22)
+    d = Dictionary.per_pixel(c.basis, c.masks)
+    cfg = hcs.SolverConfig(time_limit=None, max_iter=500, **params)
+    meas = c.y.reshape(6, 10, -1)
+    ref, st_ref = hcs.recover_cube(torch.as_tensor(meas, device="cuda"), d, cfg, algo)
+    ref = ref.cpu().numpy()
+    out = np.full((6, 10, 154), np.nan)
+    got, st = hcs.recover_cube(meas, d, cfg, algo, chunk_pixels=7, out=out)
+    assert got is out
+    np.testing.assert_array_equal(got, ref)
+    np.testing.assert_array_equal(st.iterations, st_ref.iterations)
+    np.testing.assert_array_equal(st.final_delta, st_ref.final_delta)
+    pin, st2 = hcs.recover_cube(torch.as_tensor(meas).pin_memory(), d, cfg, algo, chunk_pixels=13)
+    assert pin.is_pinned()
+    np.testing.assert_array_equal(pin.numpy(), ref)
+    assert st2.total_iterations == st_ref.total_iterations
+
+
+def test_chunked_pipeline_reports_nonfinite_from_any_chunk():
+    c = synth.generate(6, 10, 154, seed=23)
+    d = Dictionary.per_pixel(c.basis, c.masks)
+    meas = c.y.reshape(6, 10, -1).copy()
+    meas[5, 9, 3] = np.inf                      # in the last chunk only
+    with pytest.raises(ValueError):
+        hcs.recover_cube(meas, d, hcs.SolverConfig(kappa=22, time_limit=None), "gomp", chunk_pixels=8)
+    with pytest.raises(ValueError):
+        hcs.recover_cube(meas, d, hcs.SolverConfig(kappa=22, time_limit=None), "gomp",
+                         out=np.empty((6, 10, 153)))
