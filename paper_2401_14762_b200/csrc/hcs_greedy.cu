@@ -78,6 +78,7 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   if (L.bmax < 4 * kMaxN) L.bmax = 4 * kMaxN;     // also the correlation / residual / top-k key scratch
   L.gmax = csne_gram_doubles(kalloc);
   if (L.gmax < 4 * (M + 2)) L.gmax = 4 * (M + 2);  // also the pivoted fallback's vn1, vn2, z, perm
+  if (L.gmax < 136) L.gmax = 136;                   // and the post-solve top-k scratch (1 KB + 48 B)
   L.keys = 0;                   // aliases the LS region (free outside solve())
   L.vn1 = L.bmax;               // vn1 / vn2 / zt / perm alias the Gram region (free outside the
   L.vn2 = L.vn1 + M + 2;        // CSNE solve; zt is also the CoSaMP prune buffer after it)
@@ -167,9 +168,17 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
 
   // least squares on the dictionary columns `cols[0..K)` (+ y): blocked DMMA
   // Householder, exact pivoted restatement when the rank guard trips
+  // ls_b: the gathered columns (column-major, ld csne_ld(M), y as column K)
+  // stay intact after a successful CSNE solve, so the residual reads them
+  // there instead of re-gathering dictionary rows from L2
+  bool ls_ok = false, ls_shared = true;
+  const double* ls_b = S;
   auto solve = [&](const uint8_t* cols, int K) {
     const bool shared_b = K <= kalloc;
     double* B = shared_b ? S : Bglob;
+    ls_shared = shared_b;
+    ls_b = B;
+    ls_ok = false;
     const int ldb = csne_ld(M);                  // column-major; y is column K
     const int nc = csne_cols(K);
     // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
@@ -206,7 +215,10 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
     // lives in the global scratch), else in the global scratch too
     double* G = shared_b ? S + L.bmax : (csne_gram_doubles(K) <= L.bmax + L.gmax ? S : Gglob);
     const CsneScratch cs{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
-    if (ls_csne(B, ldb, M, K, sv, cs, php)) return;
+    if (ls_csne(B, ldb, M, K, sv, cs, php)) {
+      ls_ok = true;
+      return;
+    }
     const int ldp = (K + 1) | 1;
     for (int idx = tid; idx < M * (K + 1); idx += nt) {
       const int rr = idx / (K + 1), c = idx - rr * (K + 1);
@@ -336,7 +348,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         __syncthreads();
         for (int c = tid; c < ksupp; c += nt) vec[list[c]] = sv[c];
         __syncthreads();
-        cta_topk(vec, N, a.prm.kappa, g.sel, keys);
+        cta_topk_sparse(vec, N, a.prm.kappa, g.sel, keys);
         trace_store(a.st, pid, ncall, g.sel);
         if (warp == 0) bitmap_to_list(g.sel, tlist);
         __syncthreads();
@@ -347,8 +359,12 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         // keep = argmax_k(s, min(kappa, k)); zero (biht) or drop (cosamp) the rest
         const int kk = a.prm.kappa < ksupp ? a.prm.kappa : ksupp;
         double* zt = S + L.zt;
-        cta_topk(sv, ksupp, kk, g.keep, keys);
+        // scratch outside the gathered columns (kept for the residual)
+        unsigned long long* keys2 = reinterpret_cast<unsigned long long*>(ls_shared ? S + L.bmax : S);
+        cta_topk(sv, ksupp, kk, g.keep, keys2);
         trace_store(a.st, pid, ncall, g.keep);
+        // the pass's coefficients over the solve's columns, zero where not kept
+        for (int c = tid; c < ksupp; c += nt) S[L.cv + c] = bm_test(g.keep, c) ? sv[c] : 0.0;
         if (ALGO == kCosamp) {   // support = support[keep]  (stays sorted)
           if (tid < 8) g.supp[tid] = 0u;
           __syncthreads();
@@ -377,9 +393,32 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
       for (int n = tid; n < N; n += nt) x[n] = 0.0;
       __syncthreads();
       for (int c = tid; c < kx; c += nt) x[tlist[c]] = sv[c];
-      // A x over the kx support columns: lanes own rows, warps split the columns
-      {
-        double* part = S;          // free again after solve()
+      double part = 0.0;
+      int nf = 0;
+      if (ls_ok) {
+        // r = y - A x from the solve's gathered columns (y is column ks): x's
+        // support is those columns (gOMP) or the kept subset (zeros elsewhere)
+        const int ks = (ALGO == kGomp) ? kx : ksupp;
+        const double* cs_ = (ALGO == kGomp) ? sv : S + L.cv;
+        const int ld = csne_ld(M);
+        __syncthreads();
+        for (int j = tid; j < M; j += nt) {
+          double a0 = 0.0, a1 = 0.0;
+          int c = 0;
+          for (; c + 1 < ks; c += 2) {
+            a0 += ls_b[c * ld + j] * cs_[c];
+            a1 += ls_b[(c + 1) * ld + j] * cs_[c + 1];
+          }
+          if (c < ks) a0 += ls_b[c * ld + j] * cs_[c];
+          const double rn = ls_b[ks * ld + j] - (a0 + a1);
+          const double d = rn - r[j];
+          part += d * d;
+          r[j] = rn;
+        }
+      } else {
+        // A x over the kx support columns from the dictionary rows in L2: lanes
+        // own rows, warps split the columns
+        double* pbuf = S;          // free again after solve()
         double ax[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) ax[q] = 0.0;
@@ -394,18 +433,16 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (lane + 32 * q < M) part[warp * kMaxN + lane + 32 * q] = ax[q];
-      }
-      __syncthreads();
-      double part = 0.0;
-      int nf = 0;
-      for (int j = tid; j < M; j += nt) {
-        const double* pp = S + j;
-        const double axj = (pp[0] + pp[kMaxN]) + (pp[2 * kMaxN] + pp[3 * kMaxN]);
-        const double rn = ys[j] - axj;
-        const double d = rn - r[j];
-        part += d * d;
-        r[j] = rn;
+          if (lane + 32 * q < M) pbuf[warp * kMaxN + lane + 32 * q] = ax[q];
+        __syncthreads();
+        for (int j = tid; j < M; j += nt) {
+          const double* pp = S + j;
+          const double axj = (pp[0] + pp[kMaxN]) + (pp[2 * kMaxN] + pp[3 * kMaxN]);
+          const double rn = ys[j] - axj;
+          const double d = rn - r[j];
+          part += d * d;
+          r[j] = rn;
+        }
       }
       for (int c = tid; c < kx; c += nt) nf |= !isfinite(sv[c]);
       delta = sqrt(cta_sum(part, g.red));

@@ -61,6 +61,9 @@ def main():
             tot = sum(ph[:len(names)])
             print("  phases (% of CTA cycles): " + ", ".join(f"{nm} {100.0 * ph[i] / max(tot, 1):.1f}"
                                                            for i, nm in enumerate(names)))
+            nit = max(int(it.sum()), 1)
+            print(f"  CTA cycles per pixel-iteration: {tot / nit:.0f} = " + ", ".join(
+                f"{nm} {ph[i] / nit:.0f}" for i, nm in enumerate(names)))
 
 
 if __name__ == "__main__":
