@@ -196,6 +196,21 @@ class ClockSampler:
 # ------------------------------------------------------------------ GPU leg
 
 
+def _ncu_traffic(convex, algo, lab, pixels, n):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture of that launch (profiles/), when it
+    covers this kernel, configuration and cube size; else None."""
+    try:
+        rec = json.loads((ROOT / "profiles" / "ncu_traffic_r01.json").read_text())["kernels"]
+    except (OSError, ValueError, KeyError):
+        return None
+    key = (("convex_kernel<%s>" if convex else "greedy_kernel<%s>") % algo) + "|" + lab
+    r = rec.get(key)
+    if r is None or r.get("pixels") != pixels or r.get("n") != n:
+        return None
+    return int(r["dram_bytes_read"] + r["dram_bytes_write"])
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -309,7 +324,7 @@ def run_ours(args):
     work_all = float(stats[dom, 5])                 # algorithmic FLOPs of that launch, all ranks
     achieved = work_all / per_cfg[dom] / world / 1e12
     roofline = {"bound": "tensor", "unit": "TFLOP/s", "achieved": achieved, "peak": peak_tf,
-                "frac": achieved / peak_tf, "traffic": None,
+                "frac": achieved / peak_tf, "traffic": _ncu_traffic(convex, d_algo, label(d_algo, d_params), P_total, n),
                 "kernel": ("convex_kernel<%s>" if convex else "greedy_kernel<%s>") % d_algo,
                 "config": label(d_algo, d_params), "launch_ms": 1e3 * per_cfg[dom],
                 "peak_source": "FP64 DMMA m8n8k4 throughput measured on this GPU by hcs_dmma_peak_tflops "
