@@ -132,6 +132,30 @@ int hcs_lipschitz(int64_t P, int32_t N, int32_t M, const double* basis, const ui
 int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x,
                       const double* basis, double* sse_out, double* absmax_out, void* stream);
 
+/* ---- input side ------------------------------------------
+ * Synthetic spectra of the frozen generator (synth.py v1) from host-drawn
+ * parameters: f[p, b] = clip(sum_i amps[p, i] exp(-((b - centres[p, i]) /
+ * widths[p, i])^2 / 2) + noise[p, b], 0, 1); centres/widths/amps are P x 4. */
+int hcs_synth_spectra(int64_t P, int32_t N, const double* centres, const double* widths, const double* amps,
+                      const double* noise, double* f_out, void* stream);
+
+/* Sparsify + measure, the body of cli.run_sparsify / run_compress
+ * (cli.py:97-139) for the DCT basis and per-pixel masks:
+ *   c = basis^T f_p (to_sparse_domain, transform.py:40-45);
+ *   rule HCS_SPARSIFY_MAXREL:  c_i = 0 where |c_i| < factor * max|c|  (BASELINE generator);
+ *   rule HCS_SPARSIFY_MEANSTD: keep (|c_i| - mean|c|) >= factor * std|c| (transform.sparsify,
+ *                              transform.py:73-97, population std);
+ *   f_s = basis c (from_sparse_domain); y_p = f_s[mask_p] (measure, transform.py:168-173).
+ * keys (P x N, optional): mask_p = the M smallest keys' band indices, sorted (written
+ * to mask; ties to the lower index); without keys mask is an input.  coeffs_out,
+ * spectra_out (P x N) and nzero_out (device counter, incremented by the number of
+ * zeroed coefficients) may be NULL.  factor < 0 -> HCS_EINVAL (ValueError). */
+#define HCS_SPARSIFY_MAXREL 0
+#define HCS_SPARSIFY_MEANSTD 1
+int hcs_sparsify_measure(int64_t P, int32_t N, int32_t M, const double* basis, const double* f, int32_t rule,
+                         double factor, const double* keys, uint8_t* mask, double* coeffs_out, double* spectra_out,
+                         double* y_out, uint64_t* nzero_out, void* stream);
+
 /* FP64 tensor-core (DMMA m8n8k4) throughput of this GPU in TFLOP/s, best of 3
  * launches of `iters` iterations on the legacy default stream: the roofline
  * denominator for the FP64 GEMM phases (synchronises the device). */

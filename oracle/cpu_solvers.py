@@ -19,6 +19,9 @@ What is restated, and where it comes from:
 * stop rule                 solvers.py:115-127 (delta < eps > timeout > cap, delta0 = 1)
 * fista / admm / gomp / biht / cosamp  solvers.py:164-394
 * y = 0 shortcut, non-finite failure   solvers.py:145-157
+* sparsify (mean/std rule)  transform.py:73-97 (keep (|x| - mean) >= factor * std)
+* input side of a cube      cli.py:97-139 with the DCT basis, per-pixel masks and the
+                            BASELINE T max|c| rule (the synth.py v1 recipe)
 
 Deviations (all documented in DESIGN.md): real FP64 instead of complex128
 (the imaginary parts are identically zero for real bases, SURVEY.md §0 fact 4);
@@ -477,3 +480,38 @@ def psnr(reference, reconstruction):
         raise ValueError("non-positive peak")
     mse = float(np.mean((ref - rec) ** 2))
     return math.inf if mse == 0.0 else 10.0 * math.log10(peak * peak / mse)
+
+
+# ---------------------------------------------------------------- input side
+
+
+def sparsify(x, factor):
+    """transform.py:73-97: zero x_i where (|x_i| - mean|x|) < factor * std|x|
+    (population std); kept entries bit-identical.  Returns (out, mean, std,
+    zero_fraction)."""
+    if factor < 0:
+        raise ValueError("threshold factor must be >= 0")
+    x = np.asarray(x, dtype=np.float64)
+    if x.size == 0:
+        raise ValueError("cannot sparsify an empty vector")
+    mags = np.abs(x)
+    mean = float(mags.mean())
+    std = float(mags.std())
+    keep = (mags - mean) >= factor * std
+    return np.where(keep, x, 0.0), mean, std, 1.0 - float(keep.mean())
+
+
+def sparsify_measure(spectra, basis, masks, rule="maxrel", factor=0.1):
+    """Input side of a cube for the DCT basis (cli.py:97-139 restated):
+    c = basis^T f, threshold (maxrel: |c| < factor max|c| -> 0; meanstd: the
+    sparsify rule), f_s = basis c, y = f_s[mask].  Returns (coeffs, f_s, y)."""
+    c = np.asarray(spectra, dtype=np.float64) @ basis
+    mag = np.abs(c)
+    if rule == "maxrel":
+        c[mag < factor * mag.max(axis=1, keepdims=True)] = 0.0
+    else:
+        mean = mag.mean(axis=1, keepdims=True)
+        std = mag.std(axis=1, keepdims=True)
+        c[(mag - mean) < factor * std] = 0.0
+    fs = c @ basis.T
+    return c, fs, np.take_along_axis(fs, np.asarray(masks, dtype=np.intp), axis=1)

@@ -218,4 +218,31 @@ int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x, 
   return e == cudaSuccess ? HCS_OK : cuda_fail(e, "psnr_partials");
 }
 
+int hcs_synth_spectra(int64_t P, int32_t N, const double* centres, const double* widths, const double* amps,
+                      const double* noise, double* f_out, void* stream) {
+  if (P < 0) return fail(HCS_EINVAL, "negative pixel count");
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (P == 0) return HCS_OK;
+  if (!centres || !widths || !amps || !noise || !f_out) return fail(HCS_EINVAL, "null array");
+  cudaError_t e = hcs::launch_synth_spectra(P, N, centres, widths, amps, noise, f_out, num_sms(),
+                                            static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "synth_spectra");
+}
+
+int hcs_sparsify_measure(int64_t P, int32_t N, int32_t M, const double* basis, const double* f, int32_t rule,
+                         double factor, const double* keys, uint8_t* mask, double* coeffs_out, double* spectra_out,
+                         double* y_out, uint64_t* nzero_out, void* stream) {
+  if (P < 0) return fail(HCS_EINVAL, "negative pixel count");
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (M < 1 || M > N) return fail(HCS_EINVAL, "M must be in [1, N]");
+  if (rule != HCS_SPARSIFY_MAXREL && rule != HCS_SPARSIFY_MEANSTD) return fail(HCS_EINVAL, "unknown threshold rule");
+  if (!(factor >= 0)) return fail(HCS_EINVAL, "threshold factor must be >= 0");   // transform.py:85-86
+  if (P == 0) return HCS_OK;
+  if (!basis || !f || !mask || !y_out) return fail(HCS_EINVAL, "null array");
+  cudaError_t e = hcs::launch_sparsify_measure(P, N, M, rule, factor, basis, f, keys, mask, coeffs_out, spectra_out,
+                                               y_out, reinterpret_cast<unsigned long long*>(nzero_out), num_sms(),
+                                               static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "sparsify_measure");
+}
+
 }  // extern "C"

@@ -61,4 +61,12 @@ cudaError_t launch_lipschitz(long long P, int N, int M, const double* basis, con
 cudaError_t launch_psnr(long long P, int N, const double* ref, const double* x, const double* basis, double* sse,
                         double* amax, cudaStream_t stream);
 
+// hcs_input.cu
+cudaError_t launch_synth_spectra(long long P, int N, const double* centres, const double* widths, const double* amps,
+                                 const double* noise, double* f, int sms, cudaStream_t stream);
+cudaError_t launch_sparsify_measure(long long P, int N, int M, int rule, double factor, const double* basis,
+                                    const double* f, const double* keys, uint8_t* mask, double* coeffs,
+                                    double* spectra, double* y, unsigned long long* nzero, int sms,
+                                    cudaStream_t stream);
+
 }  // namespace hcs

@@ -96,10 +96,11 @@ class SyntheticCube:
         return int(self.y.shape[0])
 
 
-def _tile(n_pix, n, basis, seed, chunk=1 << 16):
-    """Spectra, coefficients, masks and measurements for one seeded tile."""
+def _draw(n_pix, n, seed):
+    """The random stream of one seeded tile (the only draws the generator
+    makes, in this order): bump centres, widths and count-masked amplitudes
+    (n_pix x 4), additive noise and mask keys (n_pix x n)."""
     rng = np.random.default_rng(seed)
-    m = measured_count(n)
     counts = rng.integers(1, 5, size=n_pix)
     centres = rng.uniform(0.0, float(n), size=(n_pix, 4))
     widths = rng.uniform(5.0, 40.0, size=(n_pix, 4))
@@ -107,6 +108,13 @@ def _tile(n_pix, n, basis, seed, chunk=1 << 16):
     amps[np.arange(4)[None, :] >= counts[:, None]] = 0.0
     noise = rng.normal(0.0, 0.01, size=(n_pix, n))
     keys = rng.random((n_pix, n))
+    return centres, widths, amps, noise, keys
+
+
+def _tile(n_pix, n, basis, seed, chunk=1 << 16):
+    """Spectra, coefficients, masks and measurements for one seeded tile."""
+    m = measured_count(n)
+    centres, widths, amps, noise, keys = _draw(n_pix, n, seed)
 
     bands = np.arange(n, dtype=np.float64)
     coeffs = np.empty((n_pix, n))
@@ -179,6 +187,98 @@ def generate(x_dim, y_dim, n, seed=0, tiles=(1, 1), x_range=None, workers=1):
         coeffs[idx], spectra[idx], masks[idx], y[idx] = c[keep], f[keep], mk[keep], yy[keep]
     return SyntheticCube(basis=basis, coeffs=coeffs, spectra=spectra, masks=masks, y=y,
                          shape=(rows, y_dim), seeds=tuple(s for _, _, s in specs))
+
+
+@dataclass
+class DeviceCube:
+    """A synthetic cube generated on the GPU (generate_device): the same
+    arrays as SyntheticCube, as CUDA tensors (coeffs only when requested)."""
+
+    basis: np.ndarray
+    spectra: object
+    masks: object
+    y: object
+    coeffs: object
+    shape: tuple
+    seeds: tuple
+    zero_fraction: float
+    version: str = GENERATOR_VERSION
+
+    @property
+    def n(self):
+        return int(self.basis.shape[0])
+
+    @property
+    def m(self):
+        return int(self.masks.shape[1])
+
+    @property
+    def n_pixels(self):
+        return int(self.y.shape[0])
+
+
+def generate_device(x_dim, y_dim, n, seed=0, tiles=(1, 1), x_range=None, with_coeffs=False, workers=16,
+                    device="cuda"):
+    """`generate` with the input-side step on the GPU.
+
+    The host only draws each tile's random stream (`_draw`, numpy, one thread
+    per tile); the spectra (hcs_synth_spectra), the DCT, the T max|c|
+    threshold, the reference spectra, the per-pixel masks (the M smallest
+    keys) and the measurements (hcs_sparsify_measure) are computed on the
+    device.  Same cube as `generate` up to FP64 rounding (exp and the DCT
+    GEMMs sum in a different order; tests/test_gpu_input.py bounds it), with
+    identical masks.
+    """
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import sparsify as sp
+
+    if n > 256:
+        raise ValueError("band indices are stored as uint8: n must be <= 256")
+    tx, ty = tiles
+    if x_dim % tx or y_dim % ty:
+        raise ValueError("tiles must divide the cube")
+    x0, x1 = x_range if x_range is not None else (0, x_dim)
+    if not 0 <= x0 <= x1 <= x_dim:
+        raise ValueError("bad x_range")
+    bx, by = x_dim // tx, y_dim // ty
+    basis = dct_basis(n)
+    m = measured_count(n)
+    rows = x1 - x0
+    P = rows * y_dim
+    dev = torch.device(device)
+    basis_d = torch.as_tensor(basis, device=dev)
+    spectra = torch.empty((P, n), dtype=torch.float64, device=dev)
+    masks = torch.empty((P, m), dtype=torch.uint8, device=dev)
+    y = torch.empty((P, m), dtype=torch.float64, device=dev)
+    coeffs = torch.empty((P, n), dtype=torch.float64, device=dev) if with_coeffs else None
+    jobs = [(i, j, max(x0, i * bx), min(x1, (i + 1) * bx)) for i in range(tx) for j in range(ty)]
+    jobs = [jb for jb in jobs if jb[2] < jb[3]]
+    seeds = [seed + ty * i + j for i, j, _, _ in jobs]
+    flat = torch.arange(P, device=dev).reshape(rows, y_dim)
+    zeroed = 0
+    with ThreadPoolExecutor(max_workers=max(1, min(workers, len(jobs)))) as pool:
+        draws = [pool.submit(_draw, bx * by, n, s) for s in seeds]
+        for (i, j, lo, hi), fut in zip(jobs, draws):
+            keep = slice((lo - i * bx) * by, (hi - i * bx) * by)   # tile rows lo..hi-1
+            cen, wid, amp, noise, keys = (np.ascontiguousarray(a[keep]) for a in fut.result())
+            f = sp.synth_spectra(*(torch.as_tensor(a, device=dev) for a in (cen, wid, amp, noise)))
+            out = sp.sparsify_measure(f, basis_d, m, rule="maxrel", factor=SPARSIFY_T,
+                                      keys=torch.as_tensor(keys, device=dev), with_coeffs=with_coeffs)
+            idx = flat[lo - x0:hi - x0, j * by:(j + 1) * by].reshape(-1)
+            spectra[idx], masks[idx], y[idx] = out.spectra, out.masks, out.y
+            if with_coeffs:
+                coeffs[idx] = out.coeffs
+            zeroed += out.zeroed
+            del f, out
+    return DeviceCube(basis=basis, spectra=spectra, masks=masks, y=y, coeffs=coeffs, shape=(rows, y_dim),
+                      seeds=tuple(seeds), zero_fraction=zeroed / float(max(P * n, 1)))
+
+
+def generate_named_device(name, seed=0, x_range=None, with_coeffs=False, device="cuda"):
+    spec = dict(CUBES[name])
+    return generate_device(seed=seed, x_range=x_range, with_coeffs=with_coeffs, device=device, **spec)
 
 
 # BASELINE.json configs (shape, bands, tiling)

@@ -79,3 +79,18 @@ def test_kernel_fixtures(golden_dir):
         basis = synth.dct_basis(n)
         mask = np.sort(np.random.default_rng(seed).choice(n, synth.measured_count(n), replace=False))
         assert abs(oc.lipschitz(basis[mask, :]) - lip) <= 1e-13
+
+
+def test_oracle_sparsify_matches_reference_golden(golden_dir):
+    """oracle.sparsify vs hypercs.transform.sparsify (transform.py:73-97) outputs
+    recorded by tests/golden/make_sparsify_golden.py: bit-identical kept vectors
+    and statistics."""
+    z = np.load(golden_dir / "sparsify.npz")
+    for x, f, out, mean, std, zf in zip(z["x"], z["factor"], z["out"], z["mean"], z["std"], z["zero_fraction"]):
+        o, m, s, zz = oc.sparsify(x, float(f))
+        assert np.array_equal(o, out)
+        assert m == mean and s == std and zz == zf
+    with pytest.raises(ValueError):
+        oc.sparsify(np.array([1.0]), -0.5)
+    with pytest.raises(ValueError):
+        oc.sparsify(np.array([]), 0.1)
