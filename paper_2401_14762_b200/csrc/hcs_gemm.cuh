@@ -34,6 +34,50 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 __device__ __forceinline__ int acc_row(int w, int rb, int lane) { return 16 * w + 8 * rb + (lane >> 2); }
 __device__ __forceinline__ int acc_col(int cb, int i, int lane) { return 8 * cb + 2 * (lane & 3) + i; }
 
+// Out = Mat * In for a 32-column tile with 2 N_pad threads: warp w owns rows
+// 16 w .. 16 w + 15 (two 8-row blocks, acc[rb][cb][i] at acc_row / acc_col).
+// Mat[r][c] = basis[r N + c] (trans = false: Psi) or basis[c N + r] (trans =
+// true: Psi^T), A fragments straight from the L2-resident row-major basis,
+// prefetched 4 k-steps ahead (the streaming kernels: PSNR, sparsify/measure).
+__device__ __forceinline__ void basis_tile_gemm(const double* __restrict__ basis, int N, int KS, bool trans,
+                                                const double* In, double (&acc)[2][4][2]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+  const int r0 = 16 * w + (lane >> 2), r1 = r0 + 8;
+  const bool v0 = r0 < N, v1 = r1 < N;
+  const size_t st = trans ? (size_t)N : 1;                  // stride along k
+  const double* p0 = basis + (trans ? (size_t)r0 : (size_t)r0 * N);
+  const double* p1 = basis + (trans ? (size_t)r1 : (size_t)r1 * N);
+  double a0[4], a1[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = 4 * i + (lane & 3);
+    a0[i] = (v0 && c < N) ? __ldg(p0 + c * st) : 0.0;
+    a1[i] = (v1 && c < N) ? __ldg(p1 + c * st) : 0.0;
+  }
+  for (int ks0 = 0; ks0 < KS; ks0 += 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double* b = In + ((ks0 + i) << 7) + lane;
+      const double b0 = b[0], b1 = b[32], b2 = b[64], b3 = b[96];
+      dmma(acc[0][0], a0[i], b0);
+      dmma(acc[1][0], a1[i], b0);
+      dmma(acc[0][1], a0[i], b1);
+      dmma(acc[1][1], a1[i], b1);
+      dmma(acc[0][2], a0[i], b2);
+      dmma(acc[1][2], a1[i], b2);
+      dmma(acc[0][3], a0[i], b3);
+      dmma(acc[1][3], a1[i], b3);
+      const int c = 4 * (ks0 + 4 + i) + (lane & 3);          // k-step ks0 + i + 4
+      a0[i] = (v0 && c < N) ? __ldg(p0 + c * st) : 0.0;
+      a1[i] = (v1 && c < N) ? __ldg(p1 + c * st) : 0.0;
+    }
+  }
+}
+
 // Balanced row-block map of the slot engine.  RB = Np / 8 row blocks of 8
 // rows over min(RB, 16) warps: the first nd = RB - 16 warps own two blocks,
 // the rest one.  The DMMA pipe is per SM sub-partition (warp w runs on

@@ -126,32 +126,6 @@ __device__ __forceinline__ int col_of_reduced8(int lane) {
   return 8 * (2 * ((lane >> 2) & 1) + ((lane >> 3) & 1)) + 2 * (lane & 3) + ((lane >> 4) & 1);
 }
 
-// acc = Mat * In over 2 row blocks (rows 16 w ..), Mat[r][c] = basis[r N + c]
-// (trans = 0, Psi) or basis[c N + r] (trans = 1, Psi^T), A fragments from L2.
-__device__ __forceinline__ void basis_gemm(const double* __restrict__ basis, int N, int KS, bool trans,
-                                           const double* In, double (&acc)[2][4][2]) {
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int rb = 0; rb < 2; ++rb)
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
-  const int r0 = 16 * w + (lane >> 2), r1 = r0 + 8;
-  for (int ks = 0; ks < KS; ++ks) {
-    const int c = 4 * ks + (lane & 3);
-    double a0 = 0.0, a1 = 0.0;
-    if (c < N) {
-      if (r0 < N) a0 = __ldg(basis + (trans ? (size_t)c * N + r0 : (size_t)r0 * N + c));
-      if (r1 < N) a1 = __ldg(basis + (trans ? (size_t)c * N + r1 : (size_t)r1 * N + c));
-    }
-    const double* b = In + (ks << 7) + lane;
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb) {
-      dmma(acc[0][cb], a0, b[32 * cb]);
-      dmma(acc[1][cb], a1, b[32 * cb]);
-    }
-  }
-}
-
 struct InputArgs {
   long long P;
   int N, M, rule;
@@ -188,7 +162,7 @@ __global__ void __launch_bounds__(512, 1) sparsify_measure_kernel(InputArgs a) {
     __syncthreads();
     // ---- c = Psi^T f ----------------------------------------------------------
     double acc[2][4][2];
-    basis_gemm(a.basis, N, KS, true, In, acc);
+    basis_tile_gemm(a.basis, N, KS, true, In, acc);
     // ---- per-pixel threshold statistics over the N rows -------------------------
     double v[8];
 #pragma unroll
@@ -266,7 +240,7 @@ __global__ void __launch_bounds__(512, 1) sparsify_measure_kernel(InputArgs a) {
       }
     __syncthreads();
     // ---- f_s = Psi c_s ----------------------------------------------------------
-    basis_gemm(a.basis, N, KS, false, In, acc);
+    basis_tile_gemm(a.basis, N, KS, false, In, acc);
     __syncthreads();   // In free again: spectra rows go there (row-major 32 x Np)
 #pragma unroll
     for (int cb = 0; cb < 4; ++cb)

@@ -11,7 +11,7 @@ from paper_2401_14762_b200 import _native
 LIB = _native.load()
 PH = (ctypes.c_ulonglong * 16)()
 HAS_PH = LIB.hcs_debug_phases_ls(PH, 1) == 0
-NAMES = {3: "gather", 4: "gram", 0: "df-entry", 1: "df-col0", 2: "df-cols", 8: "df-inv", 14: "diag0fn", 11: "diag0", 12: "panels", 13: "trail+diag", 5: "chol-end", 6: "solve+refine",
+NAMES = {3: "gather", 4: "gram", 11: "diag0", 12: "panels", 13: "trail+diag", 5: "chol-end", 6: "solve+refine",
          10: "out"}
 
 
