@@ -194,19 +194,29 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
       }
       cp_async_wait_all();
     } else {
-      // global scratch: eight independent loads in flight per thread
-      const int total = nc * ldb;
-      for (int i0 = tid; i0 < total; i0 += 8 * nt) {
-        double v[8];
+      // global scratch: warp w copies columns w, w + 4, ... two at a time,
+      // lanes over rows, six independent loads in flight per thread
+      for (int c0 = warp; c0 < nc; c0 += 8) {
+#pragma unroll 1
+        for (int r0 = lane; r0 < ldb; r0 += 96) {
+          double v[2][3];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int idx = i0 + u * nt, c = idx / ldb, rr = idx - c * ldb;
-          v[u] = 0.0;
-          if (idx < total && rr < M) v[u] = c < K ? __ldg(a.basis + (size_t)msk[rr] * N + cols[c]) : (c == K ? ys[rr] : 0.0);
+          for (int u = 0; u < 2; ++u) {
+            const int c = c0 + 4 * u;
+            const int col = c < K ? cols[c] : 0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const int rr = r0 + 32 * q;
+              v[u][q] = 0.0;
+              if (c < nc && rr < M) v[u][q] = c < K ? __ldg(a.basis + (size_t)msk[rr] * N + col) : (c == K ? ys[rr] : 0.0);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              if (c0 + 4 * u < nc && r0 + 32 * q < ldb) B[(c0 + 4 * u) * ldb + r0 + 32 * q] = v[u][q];
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (i0 + u * nt < total) B[i0 + u * nt] = v[u];
       }
     }
     __syncthreads();

@@ -56,6 +56,15 @@ __host__ __device__ __forceinline__ int gtile(int bi, int bj) { return (bi * (bi
 // element (i, k), i >= k block-wise
 __device__ __forceinline__ int gel(int i, int k) { return gtile(i >> 3, k >> 3) + (k & 7) * 8 + (i & 7); }
 
+// Row a of linear index t in a lower-triangular enumeration (t = a (a + 1) / 2 + b,
+// b <= a): closed form with a one-step correction (exact for t < 2^20).
+__device__ __forceinline__ int tri_row(int t) {
+  int a = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  if ((a + 1) * (a + 2) / 2 <= t) ++a;
+  if (a * (a + 1) / 2 > t) --a;
+  return a;
+}
+
 struct CsneScratch {   // shared memory
   double* G;      // csne_gram_doubles(K)
   double* dinv;   // >= round8(K + 1): 1 / L_ii
@@ -227,8 +236,7 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
   // ---- 1. augmented Gram, lower tiles, by DMMA ----------------------------------
   const int ntiles = nbA * (nbA + 1) / 2;
   for (int t = warp; t < ntiles; t += W) {
-    int bi = 0;
-    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    const int bi = tri_row(t);
     const int bj = t - bi * (bi + 1) / 2;
     const double* ca = B + (8 * bi + (lane >> 2)) * ld + (lane & 3);
     const double* cb = B + (8 * bj + (lane >> 2)) * ld + (lane & 3);
@@ -287,8 +295,7 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
       }
     } else {
       for (int t = warp - 1; t < ntr; t += W - 1) {
-        int a = 0;
-        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        const int a = tri_row(t);
         const int bi = kb + 1 + a, bj = kb + 1 + (t - a * (a + 1) / 2);
         if (bj >= nb || (bi == kb + 1 && bj == kb + 1)) continue;
         csne_tile_update(G, bi, bj, kb);

@@ -91,6 +91,37 @@ __global__ void latency_kernel(long long* out, int iters, double a, double b) {
   }
 }
 
+
+// warps alternate: even warps DMMA m8n8k4, odd warps DFMA — do the two FP64 paths share issue bandwidth?
+__global__ void mixed_kernel(double* out, int iters, double a, double b) {
+  int w = threadIdx.x >> 5;
+  double s = 0;
+  if (w & 1) {
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters * 2; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i];
+  } else {
+    double c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { c[i][0] = i; c[i][1] = -i; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  }
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
 template <typename K>
 float time_kernel(K launch, int reps) {
   cudaEvent_t e0, e1;
@@ -159,6 +190,17 @@ int main() {
     printf(", \"lat_dmma_cyc\": %.1f, \"lat_dfma_cyc\": %.1f, \"lat_shfl_add_cyc\": %.1f, \"lat_dsqrt_add_cyc\": %.1f, \"lat_drcp_add_cyc\": %.1f",
            (double)h[0] / it, (double)h[1] / it, (double)h[2] / it, (double)h[3] / it, (double)h[4] / it);
   }
+  {
+    // mixed: 512 threads/CTA, 2 CTAs/SM; 8 DMMA warps (each 8*iters mma = 2048*8*iters FLOP... per warp 512 FLOP/mma)
+    int blocks = sms * 2, tpb = 512;
+    float ms_m = time_kernel([&] { mixed_kernel<<<blocks, tpb>>>(out, iters, 0.999, 1e-3); }, 5);
+    double dmma_flops = 2.0 * 8 * 8 * 4 * 8 * iters * (double)blocks * (tpb / 64);
+    double dfma_flops = 2.0 * 8 * 2 * iters * (double)blocks * (tpb / 2);
+    float ms_d = time_kernel([&] { dmma884_kernel<8><<<blocks, tpb / 2>>>(out, iters); }, 5);
+    printf(", \"mixed_ms\": %.3f, \"mixed_dmma_only_ms\": %.3f, \"mixed_total_tflops\": %.2f",
+           ms_m, ms_d, (dmma_flops + dfma_flops) / ms_m / 1e9);
+  }
+  CK(cudaGetLastError());
   printf("}\n");
   return 0;
 }
