@@ -213,12 +213,21 @@ def _ncu_traffic(convex, algo, lab, pixels, n):
     return int(r["dram_bytes_read"] + r["dram_bytes_write"])
 
 
+def _hbm_peak():
+    """HBM copy bandwidth of this pool (MEASURED_PEAKS.json, driver-written), else
+    the profiling recipe's fallback."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "of fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2401_14762_b200 import _native, parallel
-    from paper_2401_14762_b200.metrics import psnr_partials
+    from paper_2401_14762_b200.metrics import sse_coeff_partials
     from paper_2401_14762_b200.solvers import SolverConfig, recover_cube, solve_batch
     from paper_2401_14762_b200.transform import Dictionary
 
@@ -242,13 +251,14 @@ def run_ours(args):
     t_gen = time.perf_counter()
     if args.gen == "device":
         # input side on the GPU (hcs_synth_spectra + hcs_sparsify_measure; host draws the random stream)
-        cube = synth.generate_named_device(cube_name, x_range=(x0, x1), device=dev)
-        y_d, masks_d, spectra_d = cube.y, cube.masks, cube.spectra
+        cube = synth.generate_named_device(cube_name, x_range=(x0, x1), device=dev, with_coeffs=True)
+        y_d, masks_d, spectra_d, coeffs_d = cube.y, cube.masks, cube.spectra, cube.coeffs
     else:
         cube = synth.generate_named(cube_name, x_range=(x0, x1), workers=min(16, host_cores()))
         y_d = torch.as_tensor(cube.y, device=dev)
         masks_d = torch.as_tensor(cube.masks, device=dev)
         spectra_d = torch.as_tensor(cube.spectra, device=dev)
+        coeffs_d = torch.as_tensor(cube.coeffs, device=dev)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     P, n, m = cube.n_pixels, cube.n, cube.m
@@ -300,7 +310,9 @@ def run_ours(args):
             if record is not None:
                 record[i][1].record()
             out = b
-            psnr_partials(spectra_d, b.x, basis_d, out=psnr_d[i])
+            # PSNR's squared error in the coefficient domain (Parseval):
+            # one HBM stream over the reference and recovered coefficients
+            sse_coeff_partials(coeffs_d, b.x, out=psnr_d[i, :1])
             for f, v in enumerate(parallel.local_stats(b)):
                 stats_d[i, 1 + f] = v
             launches += b.launches + 1
@@ -368,6 +380,25 @@ def run_ours(args):
                 "per_config_tflops": {label(a, p): float(stats[i, 5]) / per_cfg[i] / world / 1e12
                                       for i, (a, p, _) in enumerate(cfgs)}}
 
+    # streaming phase: the coefficient-domain PSNR kernel alone (HBM-bound), timed
+    # with events on its stream over the last recovered cube
+    sse_tmp = torch.zeros(1, dtype=torch.float64, device=dev)
+    sse_coeff_partials(coeffs_d, out.x, out=sse_tmp)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(10):
+        sse_coeff_partials(coeffs_d, out.x, out=sse_tmp)
+    s1.record()
+    torch.cuda.synchronize()
+    t_sse = s0.elapsed_time(s1) / 10e3
+    hbm_peak, hbm_src = _hbm_peak()
+    sse_bytes = 2 * 8 * P * n
+    streaming = {"bound": "hbm", "kernel": "sse_coeff_kernel", "unit": "GB/s", "achieved": sse_bytes / t_sse / 1e9,
+                 "peak": hbm_peak, "frac": sse_bytes / t_sse / 1e9 / hbm_peak, "launch_ms": 1e3 * t_sse,
+                 "peak_source": hbm_src,
+                 "algorithmic": f"16 bytes per voxel (reference + recovered coefficient), {P} x {n} voxels per rank; "
+                                "PSNR squared error by Parseval, no spectra GEMM"}
+
     total_spectra = P_total * nsolv * args.steps
     value = total_spectra / elapsed
     per_solver = {label(a, p): P_total / t for (a, p, _), t in zip(cfgs, per_cfg)}
@@ -433,7 +464,7 @@ def run_ours(args):
                        "parallelism": f"pixel-row slabs x{world}", "l2": "inputs (1.28 GB/step) > 126 MB L2; no flush"},
             "per_solver": per_solver, "quality": quality,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk, "generation_s": t_gen, "input_side": input_side,
+            "clocks": clk, "generation_s": t_gen, "input_side": input_side, "streaming": streaming,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -132,6 +132,14 @@ int hcs_lipschitz(int64_t P, int32_t N, int32_t M, const double* basis, const ui
 int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x,
                       const double* basis, double* sse_out, double* absmax_out, void* stream);
 
+/* Coefficient-domain PSNR partial: sse_out[0] += sum over
+ * P x N of (ref_coeffs - x)^2.  For an orthonormal basis this equals the
+ * spectral-domain SSE of hcs_psnr_partials (Parseval) with no GEMM: an HBM
+ * stream of 16 bytes per voxel.  The peak max|ref spectra| is input-derived
+ * (hcs_psnr_partials or the caller's reduction). */
+int hcs_sse_coeff_partials(int64_t P, int32_t N, const double* ref_coeffs, const double* x, double* sse_out,
+                           void* stream);
+
 /* ---- input side ------------------------------------------
  * Synthetic spectra of the frozen generator (synth.py v1) from host-drawn
  * parameters: f[p, b] = clip(sum_i amps[p, i] exp(-((b - centres[p, i]) /

@@ -20,6 +20,7 @@ EXPORTS = (
     "hcs_abi_version", "hcs_last_error", "hcs_workspace_bytes", "hcs_recover", "hcs_recover_status",
     "hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta", "hcs_lipschitz",
     "hcs_psnr_partials", "hcs_dmma_peak_tflops", "hcs_synth_spectra", "hcs_sparsify_measure",
+    "hcs_sse_coeff_partials",
 )
 
 
@@ -84,12 +85,14 @@ def load(path=None):
     lib.hcs_residual_delta.argtypes = [i64, i32, vp, vp, vp, vp]
     lib.hcs_lipschitz.argtypes = [i64, i32, i32, vp, vp, vp, vp]
     lib.hcs_psnr_partials.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp]
+    lib.hcs_sse_coeff_partials.argtypes = [i64, i32, vp, vp, vp, vp]
     lib.hcs_synth_spectra.argtypes = [i64, i32, vp, vp, vp, vp, vp, vp]
     lib.hcs_sparsify_measure.argtypes = [i64, i32, i32, vp, vp, i32, dbl, vp, vp, vp, vp, vp, vp, vp]
     lib.hcs_dmma_peak_tflops.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     lib.hcs_dmma_peak_tflops.restype = ctypes.c_int
     for name in ("hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta",
-                 "hcs_lipschitz", "hcs_psnr_partials", "hcs_synth_spectra", "hcs_sparsify_measure"):
+                 "hcs_lipschitz", "hcs_psnr_partials", "hcs_synth_spectra", "hcs_sparsify_measure",
+                 "hcs_sse_coeff_partials"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -218,6 +218,17 @@ int hcs_psnr_partials(int64_t P, int32_t N, const double* ref, const double* x, 
   return e == cudaSuccess ? HCS_OK : cuda_fail(e, "psnr_partials");
 }
 
+int hcs_sse_coeff_partials(int64_t P, int32_t N, const double* ref_coeffs, const double* x, double* sse_out,
+                           void* stream) {
+  if (P < 0) return fail(HCS_EINVAL, "negative pixel count");
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (P == 0) return HCS_OK;
+  if (!ref_coeffs || !x || !sse_out) return fail(HCS_EINVAL, "null array");
+  cudaError_t e = hcs::launch_sse_coeff(P * (long long)N, ref_coeffs, x, sse_out, num_sms(),
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? HCS_OK : cuda_fail(e, "sse_coeff_partials");
+}
+
 int hcs_synth_spectra(int64_t P, int32_t N, const double* centres, const double* widths, const double* amps,
                       const double* noise, double* f_out, void* stream) {
   if (P < 0) return fail(HCS_EINVAL, "negative pixel count");

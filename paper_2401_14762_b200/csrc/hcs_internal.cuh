@@ -60,6 +60,8 @@ cudaError_t launch_lipschitz(long long P, int N, int M, const double* basis, con
                              cudaStream_t stream);
 cudaError_t launch_psnr(long long P, int N, const double* ref, const double* x, const double* basis, double* sse,
                         double* amax, cudaStream_t stream);
+cudaError_t launch_sse_coeff(long long n, const double* a, const double* b, double* sse, int sms,
+                             cudaStream_t stream);
 
 // hcs_input.cu
 cudaError_t launch_synth_spectra(long long P, int N, const double* centres, const double* widths, const double* amps,

@@ -55,6 +55,26 @@ def psnr_partials(ref_spectra, coeffs, basis, out=None, stream=None):
     return out
 
 
+def sse_coeff_partials(ref_coeffs, coeffs, out=None, stream=None):
+    """Device SSE of the recovered spectra in the coefficient domain (CUDA tensors).
+
+    For the orthonormal DCT-II basis ||f_ref - Psi x||^2 = ||c_ref - x||^2
+    (Parseval), so PSNR needs only the sparsified reference coefficients and the
+    recovered ones: one HBM stream (hcs_sse_coeff_partials), no spectra GEMM.
+    Accumulates into ``out[0]`` (a float64 CUDA tensor) when given."""
+    import torch
+    if ref_coeffs.shape != coeffs.shape or ref_coeffs.dtype != torch.float64 or coeffs.dtype != torch.float64:
+        raise ValueError("ref_coeffs and coeffs must be float64 arrays of the same shape")
+    if not (ref_coeffs.is_contiguous() and coeffs.is_contiguous()):
+        raise ValueError("ref_coeffs and coeffs must be contiguous")
+    P, n = int(ref_coeffs.shape[0]), int(ref_coeffs.shape[1])
+    if out is None:
+        out = torch.zeros(1, dtype=torch.float64, device=ref_coeffs.device)
+    nat.check(nat.load().hcs_sse_coeff_partials(P, n, nat.ptr(ref_coeffs), nat.ptr(coeffs), ctypes_ptr(out, 0),
+                                                nat.stream_handle(stream)))
+    return out
+
+
 def ctypes_ptr(t, i):
     import ctypes
     return ctypes.c_void_p(t.data_ptr() + i * t.element_size())

@@ -143,3 +143,33 @@ def test_empty_and_invalid_inputs():
         sp.sparsify_measure(np.zeros((2, 16)), b, 6, rule="median", masks=np.zeros((2, 6), np.uint8))
     with pytest.raises(ValueError):
         sp.sparsify_measure(np.zeros((2, 16)), b, 6)
+
+
+@pytest.mark.parametrize("P,n,offset", [(5000, 224, 0), (777, 198, 0), (333, 154, 1), (1, 1, 0)])
+def test_sse_coeff_partials_parseval(P, n, offset):
+    """Coefficient-domain SSE equals the spectral-domain SSE
+    of the reference's psnr (metrics.py:30-55) for the orthonormal DCT-II basis:
+    ||f_ref - Psi x||^2 = ||c_ref - x||^2.  offset=1 exercises the unaligned
+    (scalar) path; n*P odd exercises the double2 tail."""
+    from paper_2401_14762_b200.metrics import psnr_partials, sse_coeff_partials
+    rng = np.random.default_rng(P + n)
+    basis = synth.dct_basis(n)
+    c = rng.standard_normal((P, n)) * (rng.random((P, n)) < 0.1)
+    x = c + 1e-3 * rng.standard_normal((P, n))
+    f = c @ basis.T                       # f_p = Psi c_p
+    dev = torch.device("cuda")
+    flat_c = torch.as_tensor(np.concatenate([np.zeros(offset), c.ravel()]), device=dev)[offset:].view(P, n)
+    flat_x = torch.as_tensor(np.concatenate([np.zeros(offset), x.ravel()]), device=dev)[offset:].view(P, n)
+    got = float(sse_coeff_partials(flat_c, flat_x).item())
+    want = float(np.sum((c - x) ** 2))
+    assert abs(got - want) <= 1e-12 * want
+    spec = psnr_partials(torch.as_tensor(f, device=dev), torch.as_tensor(x, device=dev),
+                         torch.as_tensor(basis, device=dev)).cpu().numpy()
+    assert abs(got - spec[0]) <= 1e-9 * spec[0]
+
+
+def test_sse_coeff_partials_rejects_mismatch():
+    from paper_2401_14762_b200.metrics import sse_coeff_partials
+    a = torch.zeros((4, 8), dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        sse_coeff_partials(a, torch.zeros((4, 9), dtype=torch.float64, device="cuda"))

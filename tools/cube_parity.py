@@ -1,0 +1,191 @@
+"""Whole-cube parity at BASELINE.json's full config sizes.
+
+    python tools/cube_parity.py [--only cfg1,cfg3] [--jobs N] [--skip-slow]
+
+For every BASELINE configuration whose cube the oracle can finish in minutes
+(cfg1 jasper 100x100x198, cfg2, cfg3 china 420x140x154, cfg4 salinas
+512x217x224, and the scaling run's ten solver configurations on its 512x217
+tile 0), the cube is generated on the host (synth.generate_named: exactly the
+arrays the oracle reads), recovered on the GPU (hcs_recover) and by the CPU
+oracle over ALL pixels, and compared: cube PSNR (|dB| <= 0.01 unless both are
+in the roundoff regime), per-pixel coefficients (1e-9 norm-relative),
+iteration / converged / failed_at agreement.  Pixels that disagree are the
+tie-exception candidates of §8(c) (the per-call tie classification with
+forced-selection replay runs on samples in tests/ and tools/parity_report.py);
+their share of the cube's squared error is reported so a PSNR difference can
+be traced to them.  Diagnostics only: the oracle is test infrastructure.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from oracle import cpu_solvers as oc  # noqa: E402
+from paper_2401_14762_b200 import synth  # noqa: E402
+
+# (tag, cube, algo, params, cap) -- BASELINE.json configs 1-4 and config 5's solvers on tile 0
+CASES = [
+    ("cfg1", "jasper", "gomp", dict(kappa=24, atoms_per_iter=4), None),
+    ("cfg2", "jasper", "fista", dict(lam=100.0), 5000),
+    ("cfg2", "jasper", "admm", dict(lam=100.0, alpha=1.8), 5000),
+    ("cfg2", "jasper", "fista", dict(lam=0.1), 5000),
+    ("cfg2", "jasper", "admm", dict(lam=0.1, alpha=1.8), 5000),
+    ("cfg3", "china", "biht", dict(kappa=22, mu=0.1), 2000),
+    ("cfg3", "china", "gomp", dict(kappa=22, atoms_per_iter=4), None),
+    ("cfg4", "salinas", "cosamp", dict(kappa=33), 2000),
+    ("cfg5t0", "salinas", "gomp", dict(kappa=27, atoms_per_iter=5), None),
+    ("cfg5t0", "salinas", "gomp", dict(kappa=33, atoms_per_iter=6), None),
+    ("cfg5t0", "salinas", "biht", dict(kappa=27, mu=0.1), 2000),
+    ("cfg5t0", "salinas", "biht", dict(kappa=33, mu=0.1), 2000),
+    ("cfg5t0", "salinas", "cosamp", dict(kappa=27), 2000),
+    ("cfg5t0", "salinas", "fista", dict(lam=0.1), 5000),
+    ("cfg5t0", "salinas", "fista", dict(lam=100.0), 5000),
+    ("cfg5t0", "salinas", "admm", dict(lam=100.0, alpha=1.8), 5000),
+    ("cfg5t0", "salinas", "admm", dict(lam=0.1, alpha=1.8), 5000),
+]
+SLOW = {("salinas", "admm", 0.1)}
+
+
+def psnr_parts(ref_spectra, basis, x):
+    rec = x @ basis.T
+    d = ref_spectra - rec
+    per_pixel = np.einsum("pn,pn->p", d, d)
+    return per_pixel, float(np.max(np.abs(ref_spectra)))
+
+
+def db(sse, peak, count):
+    mse = sse / count
+    return float("inf") if mse == 0 else 10.0 * np.log10(peak * peak / mse)
+
+
+def classify(algo, c, bad_mask, cfg, ocfg, pool, jobs):
+    """§8(c) tie classification of the disagreeing pixels: selection traces of
+    both sides, first divergent argmax_k call, roundoff-degeneracy on the
+    oracle side, forced-selection replay."""
+    import torch
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from parity import compare
+    from test_gpu_parity import decode_trace, make_replay
+
+    from paper_2401_14762_b200.solvers import solve_batch
+
+    idx = np.flatnonzero(bad_mask)
+    y, masks = np.ascontiguousarray(c.y[idx]), np.ascontiguousarray(c.masks[idx])
+    dev = torch.device("cuda")
+    b = solve_batch(algo, torch.as_tensor(y, device=dev), torch.as_tensor(masks, device=dev),
+                    torch.as_tensor(c.basis, device=dev), cfg, trace_calls=64)
+    torch.cuda.synchronize()
+    got = dict(x=b.x.cpu().numpy(), iterations=b.iterations.cpu().numpy(),
+               converged=b.converged.cpu().numpy().astype(bool), failed_at=b.failed_at.cpu().numpy(),
+               trace=decode_trace((b.trace, b.trace_len), c.n))
+    ref = oc.solve_cube(algo, c.basis, y, masks, ocfg, jobs=jobs, pool=pool, trace=True, chunk=16)
+    rep = compare(dict(x=ref.x, iterations=ref.iterations, converged=ref.converged, failed_at=ref.failed_at), got, y,
+                  ref.traces, got["trace"], algo, replay=make_replay(algo, c.basis, y, masks, ocfg))
+    calls = {}
+    for t in rep["ties"]:
+        calls[t.get("call")] = calls.get(t.get("call"), 0) + 1
+    return {"ties": len(rep["ties"]), "ties_replay_ok": sum(1 for t in rep["ties"] if t.get("replay_ok")),
+            "real_mismatches": len(rep["bad"]), "tie_first_divergence_calls": calls,
+            "mismatch_examples": [dict(e, pixel=int(idx[e["pixel"]])) for e in rep["bad"][:3]]}
+
+
+def main():
+    import torch
+
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--jobs", type=int, default=len(os.sched_getaffinity(0)))
+    ap.add_argument("--skip-slow", action="store_true")
+    ap.add_argument("--ties", action="store_true", help="classify the disagreeing greedy pixels (traces + replay)")
+    ap.add_argument("--perturb", action="store_true", help="oracle PSNR under a 1-ulp perturbation of y")
+    args = ap.parse_args()
+    only = set(args.only.split(",")) if args.only else None
+    dev = torch.device("cuda")
+    cubes = {}
+    pool = ProcessPoolExecutor(max_workers=args.jobs, initializer=oc.single_thread_blas)
+    for tag, cube_name, algo, params, cap in CASES:
+        if only and tag not in only:
+            continue
+        if args.skip_slow and (cube_name, algo, params.get("lam")) in SLOW:
+            continue
+        if cube_name not in cubes:
+            t = time.perf_counter()
+            cubes[cube_name] = synth.generate_named(cube_name, workers=min(16, args.jobs))
+            print(f"[parity] {cube_name}: {cubes[cube_name].n_pixels} px generated in {time.perf_counter() - t:.1f}s",
+                  file=sys.stderr, flush=True)
+        c = cubes[cube_name]
+        cfg = SolverConfig(time_limit=None, max_iter=cap, **params)
+        b = solve_batch(algo, torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev),
+                        torch.as_tensor(c.basis, device=dev), cfg)
+        torch.cuda.synchronize()
+        gx = b.x.cpu().numpy()
+        git = b.iterations.cpu().numpy()
+        gconv = b.converged.cpu().numpy().astype(bool)
+        gfail = b.failed_at.cpu().numpy()
+        ocfg = oc.OracleConfig(max_iter=cap or 0, **params)
+        t = time.perf_counter()
+        ref = oc.solve_cube(algo, c.basis, c.y, c.masks, ocfg, jobs=args.jobs, pool=pool, chunk=256)
+        t_or = time.perf_counter() - t
+        P = c.n_pixels
+        nr = np.linalg.norm(ref.x, axis=1)
+        err = np.linalg.norm(gx - ref.x, axis=1)
+        rel = np.where(nr > 0, err / np.maximum(nr, 1e-300), err)
+        coef_bad = np.where(nr > 0, rel > 1e-9, err > 1e-12)
+        it_bad = git != ref.iterations
+        conv_bad = gconv != ref.converged
+        fail_bad = gfail != ref.failed_at
+        any_bad = coef_bad | it_bad | conv_bad | fail_bad
+        sse_g, peak = psnr_parts(c.spectra, c.basis, gx)
+        sse_r, _ = psnr_parts(c.spectra, c.basis, ref.x)
+        cnt = c.spectra.size
+        p_g, p_r = db(sse_g.sum(), peak, cnt), db(sse_r.sum(), peak, cnt)
+        share_r = float(sse_r[any_bad].sum() / max(sse_r.sum(), 1e-300))
+        share_g = float(sse_g[any_bad].sum() / max(sse_g.sum(), 1e-300))
+        ok = ~any_bad
+        # PSNR over the pixels that agree (the tie-exception candidates removed)
+        p_g_ok = db(sse_g[ok].sum(), peak, ok.sum() * c.n)
+        p_r_ok = db(sse_r[ok].sum(), peak, ok.sum() * c.n)
+        line = {
+            "config": tag, "cube": cube_name, "pixels": P, "algo": algo,
+            "params": {k: v for k, v in params.items()}, "cap": cap,
+            "psnr_gpu_db": p_g, "psnr_oracle_db": p_r, "dpsnr_db": p_g - p_r,
+            "psnr_within_0.01dB": bool(abs(p_g - p_r) <= 0.01 or (p_g > 200 and p_r > 200)),
+            "disagreeing_pixels": int(any_bad.sum()), "disagreeing_pct": 100.0 * any_bad.mean(),
+            "coef_mismatch": int(coef_bad.sum()), "iteration_mismatch": int(it_bad.sum()),
+            "converged_mismatch": int(conv_bad.sum()), "failed_mismatch": int(fail_bad.sum()),
+            "worst_rel_agreeing": float(rel[ok].max()) if ok.any() else None,
+            "median_rel": float(np.median(rel)),
+            "sse_share_of_disagreeing_oracle": share_r, "sse_share_of_disagreeing_gpu": share_g,
+            "psnr_agreeing_gpu_db": p_g_ok, "psnr_agreeing_oracle_db": p_r_ok,
+            "iters_gpu": int(git.sum()), "iters_oracle": int(ref.iterations.sum()),
+            "oracle_s": t_or, "oracle_cores": args.jobs,
+        }
+        if args.ties and algo in ("gomp", "biht", "cosamp") and any_bad.any():
+            line.update(classify(algo, c, any_bad, cfg, ocfg, pool, args.jobs))
+        if args.perturb and any_bad.any():
+            # the oracle's own sensitivity: y scaled by (1 + 2^-52 N(0,1)), a 1-ulp input change
+            rng = np.random.default_rng(7)
+            yp = c.y * (1.0 + 2.0 ** -52 * rng.standard_normal(c.y.shape))
+            refp = oc.solve_cube(algo, c.basis, yp, c.masks, ocfg, jobs=args.jobs, pool=pool, chunk=256)
+            sse_p, _ = psnr_parts(c.spectra, c.basis, refp.x)
+            p_p = db(sse_p.sum(), peak, cnt)
+            line.update({"psnr_oracle_1ulp_db": p_p, "dpsnr_oracle_1ulp_db": p_p - p_r,
+                         "oracle_1ulp_iteration_flips": int((refp.iterations != ref.iterations).sum())})
+        print(json.dumps(line), flush=True)
+    pool.shutdown()
+
+
+if __name__ == "__main__":
+    main()
