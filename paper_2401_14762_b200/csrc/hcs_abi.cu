@@ -121,7 +121,9 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
 
   if (algo == HCS_FISTA || algo == HCS_ADMM) {
     const int Np = pad16(N);
-    if (hcs::convex_smem_bytes(algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm, Np, M) > (size_t)kSmemPerBlock)
+    const int calgo = algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm;
+    const int slots = hcs::convex_slots(calgo, Np, M);
+    if (hcs::convex_smem_bytes(calgo, Np, M, slots) > (size_t)kSmemPerBlock)
       return fail(HCS_EINVAL, "convex solvers: 32 pixel slots of N = " + std::to_string(N) + ", M = " +
                                   std::to_string(M) + " exceed the 227 KB shared memory of one SM");
     double* fragS = reinterpret_cast<double*>(ws + kHeader);
@@ -129,16 +131,18 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     double* u0 = reinterpret_cast<double*>(ws + kHeader + 2 * align256(sizeof(double) * (size_t)Np * Np));
     double* lip = reinterpret_cast<double*>(ws + kHeader + 2 * align256(sizeof(double) * (size_t)Np * Np) +
                                             align256(sizeof(double) * (size_t)Np));
-    e = hcs::launch_prep_basis(basis, N, Np, fragS, fragT, u0, stream);
+    e = hcs::launch_prep_basis(basis, N, Np, fragS, fragT, u0, slots, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_basis_kernel");
     if (algo == HCS_FISTA) {
       e = hcs::launch_lipschitz_prepass(P, M, mask, u0, lip, sms, stream);
       if (e != cudaSuccess) return cuda_fail(e, "lipschitz_prepass_kernel");
     }
     hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, lip, x_out, st, pr, counter, err};
-    const long long tiles = (P + hcs::kSlots - 1) / hcs::kSlots;
-    const int grid = (int)(tiles < sms ? tiles : sms);
-    e = hcs::launch_convex(algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm, args, grid, stream);
+    // persistent: one CTA (32 slots) or two CTAs (16 slots each) per SM
+    const long long tiles = (P + slots - 1) / slots;
+    const long long ctas = slots == 32 ? sms : 2LL * sms;
+    const int grid = (int)(tiles < ctas ? tiles : ctas);
+    e = hcs::launch_convex(calgo, args, slots, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "convex_kernel");
     return HCS_OK;
   }

@@ -27,6 +27,7 @@
 // two GEMMs per iteration and the residual for free.
 #include "hcs_gemm.cuh"
 #include "hcs_internal.cuh"
+#include <cstdlib>
 
 namespace hcs {
 
@@ -36,18 +37,26 @@ enum { kEmpty = 0, kActive = 1 };
 __device__ unsigned long long g_phase_cx[16];
 #endif
 
+template <int SL>
 struct SlotState {
-  long long pid[kSlots];
-  long long rpid[kSlots];
-  long long start[kSlots];
-  long long npid[kSlots];     // staged next pixel of the slot (>= P: none)
-  double slip[kSlots];        // its Lipschitz constant (fista)
-  double t[kSlots], tn[kSlots], betan[kSlots];
-  double inv_l[kSlots], thr[kSlots];
-  int status[kSlots], iter[kSlots], flag[kSlots], rfail[kSlots], retired[kSlots], moff[kSlots], need_pf[kSlots];
+  long long pid[SL];
+  long long rpid[SL];
+  long long start[SL];
+  long long npid[SL];     // staged next pixel of the slot (>= P: none)
+  double slip[SL];        // its Lipschitz constant (fista)
+  double t[SL], tn[SL], betan[SL];
+  double inv_l[SL], thr[SL];
+  int status[SL], iter[SL], flag[SL], rfail[SL], retired[SL], moff[SL], need_pf[SL];
   int nact[2];
   int exhausted;
 };
+
+// Slot-column layout of the GEMM input buffers: 32 slots (one CTA per SM) or 16
+// (two CTAs per SM, hcs_gemm.cuh)
+template <int SL>
+__device__ __forceinline__ int slot_idx(int k, int s) {
+  if constexpr (SL == 32) return in_idx(k, s); else return in_idx16(k, s);
+}
 
 __host__ __device__ __forceinline__ int stage_mask_bytes(int M) { return ((M + 7) & ~7) + 8; }
 
@@ -56,8 +65,8 @@ __host__ __device__ __forceinline__ int stage_mask_bytes(int M) { return ((M + 7
 // staging area with cp.async: the refill that consumes it, usually many ticks
 // later, finds the data in shared memory instead of waiting on HBM.  Called
 // by the owning warp (cp.async completion is per thread).
-template <int ALGO>
-__device__ void prefetch_slot(const ConvexArgs& a, SlotState& ss, double* sy, uint8_t* sm, int s) {
+template <int ALGO, int SL>
+__device__ void prefetch_slot(const ConvexArgs& a, SlotState<SL>& ss, double* sy, uint8_t* sm, int s) {
   const int lane = threadIdx.x & 31;
   const int M = a.M, Mm = stage_mask_bytes(M);
   long long pid = 0;
@@ -93,15 +102,15 @@ __device__ void prefetch_slot(const ConvexArgs& a, SlotState& ss, double* sy, ui
 // the next pixel is staged right after the slot phase (need_pf), where the
 // queue atomic's round trip overlaps the other warps' GEMM work.  Called by
 // the owning warp.
-template <int ALGO>
-__device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, double* bufB, double* ys, double* r,
+template <int ALGO, int SL>
+__device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA, double* bufB, double* ys, double* r,
                             uint8_t* pos, double* sy, uint8_t* sm, int s) {
   const int lane = threadIdx.x & 31;
   const int M = a.M, N = a.N, Np = a.Np, Mm = stage_mask_bytes(M);
   uint8_t* ps = pos + s * kMaxN;
   for (int n = lane; n < Np; n += 32) {
-    bufA[in_idx(n, s)] = 0.0;
-    if (ALGO == kFista) bufB[in_idx(n, s)] = 0.0;   // z_0 = 0
+    bufA[slot_idx<SL>(n, s)] = 0.0;
+    if (ALGO == kFista) bufB[slot_idx<SL>(n, s)] = 0.0;   // z_0 = 0
   }
   for (;;) {
     cp_async_wait_all();
@@ -137,7 +146,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, do
         if (a.st.work) a.st.work[pid] = 0.0;
       }
       __syncwarp();
-      prefetch_slot<ALGO>(a, ss, sy, sm, s);
+      prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       continue;
     }
     if (ALGO == kAdmm && bad && lane == 0) atomicOr(a.err, 1);   // cho_solve would raise
@@ -156,7 +165,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, do
         if (a.st.work) a.st.work[pid] = 0.0;
       }
       __syncwarp();
-      prefetch_slot<ALGO>(a, ss, sy, sm, s);
+      prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       continue;
     }
     for (int b = lane; b < kMaxN; b += 32) ps[b] = 0xFF;
@@ -165,7 +174,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, do
     for (int j = lane; j < M; j += 32) {
       const int row = mrow[j];
       ps[row] = (uint8_t)j;
-      if (ALGO == kFista) bufA[in_idx(row, s)] = -ys[s * M + j];
+      if (ALGO == kFista) bufA[slot_idx<SL>(row, s)] = -ys[s * M + j];
     }
     if (lane == 0) {
       ss.pid[s] = pid;
@@ -188,7 +197,8 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState& ss, double* bufA, do
 
 // Stop rule after an iteration (solvers.py:115-127 evaluated before the next
 // pass) plus the non-finite check (solvers.py:155-157).  Lane 0 of the owner.
-__device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState& ss, int s, double delta,
+template <int SL>
+__device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState<SL>& ss, int s, double delta,
                                                  bool admm, double gap2) {
   int it = ss.iter[s] + 1;
   ss.iter[s] = it;
@@ -212,47 +222,52 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState&
   }
 }
 
-// One tick = one solver iteration of all 32 slots:
+// One tick = one solver iteration of all SL slots:
 //   slot phase (stop rule on the partial sums, refill)                | barrier
 //   writeback of retired slots; GEMM 1 (reads A); epilogue 1 (writes B) | barrier
 //   GEMM 2 (reads B); epilogue 2 (writes A for the next tick)          | barrier
 // (admm: A = z - w, B = u'; each buffer is written only after every warp is
 // done reading it, so no barrier sits between a GEMM and its epilogue.
-// fista: A holds g, then x_{k+1}, then the next g, B holds z (registers are
-// full at 128), two more barriers.)  Per-element iterates stay in registers
-// in the accumulator layout: fista p0 = x_k; admm p1 = w (z goes to x_out
-// every pass).
-// Residual-delta and ADMM-gap sums are reduced per warp (col_reduce8) into
+// fista: A holds g, then x_{k+1}, then the next g, B holds z, two more
+// barriers.)  Per-element iterates stay in registers in the accumulator
+// layout: fista p0 = x_k; admm p1 = w (z goes to x_out every pass).
+// Residual-delta and ADMM-gap sums are reduced per warp (col_reduce) into
 // part[], summed in fixed order by the slot's owner: deterministic.
-// 13..16 warps put 4 warps on one SM sub-partition (16K registers): <= 128 regs.
-template <int ALGO, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
+// SL = 32: one CTA per SM, up to 16 warps of 1-2 row blocks x 4 column blocks
+// (<= 128 registers).  SL = 16: two CTAs per SM of 8 warps, up to 4 row blocks
+// x 2 column blocks each; the two CTAs drift out of phase so that one's
+// epilogues and slot phase overlap the other's GEMMs on the DMMA pipe.
+template <int ALGO, int SL, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
+  constexpr int CB = SL / 8;                  // 8-column blocks
+  constexpr int MAXRB = (SL == 32) ? 2 : 4;   // row blocks per warp
+  constexpr int NV = 2 * CB;                  // per-lane column partials
   extern __shared__ __align__(16) unsigned char smraw[];
   const int Np = a.Np, M = a.M, N = a.N, KS = Np >> 2;
   const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int rb0, nrb;
-  warp_rows(Np >> 3, w, rb0, nrb);
+  if constexpr (SL == 32) warp_rows(Np >> 3, w, rb0, nrb); else warp_rows16(Np >> 3, W, w, rb0, nrb);
   const int row0 = 8 * rb0 + (lane >> 2);   // element row of acc[rb] is row0 + 8 rb
-  double* bufA = reinterpret_cast<double*>(smraw);      // Np * 32: fista g / x_{k+1}, admm z - w
-  double* bufB = bufA + Np * kSlots;                    // Np * 32: fista z, admm u'
-  double* ys = bufB + Np * kSlots;                      // 32 * M
-  double* r = ys + kSlots * M;                          // 32 * M
-  double* partD = r + kSlots * M;                       // 16 * 32 residual-delta partials
-  double* partG = partD + 16 * kSlots;                  // 16 * 32 admm gap partials
-  double* sy = partG + 16 * kSlots;                     // 32 * M staged next measurements
-  SlotState& ss = *reinterpret_cast<SlotState*>(sy + kSlots * M);
-  uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // 32 * 256: row -> measurement index
-  uint8_t* sm = pos + kSlots * kMaxN;                   // 32 * stage_mask_bytes(M) staged mask rows
-  const int cred = col_of_reduced(lane);
+  double* bufA = reinterpret_cast<double*>(smraw);      // Np * SL: fista g / x_{k+1}, admm z - w
+  double* bufB = bufA + Np * SL;                        // Np * SL: fista z, admm u'
+  double* ys = bufB + Np * SL;                          // SL * M
+  double* r = ys + SL * M;                              // SL * M
+  double* partD = r + SL * M;                           // 16 * SL residual-delta partials
+  double* partG = partD + 16 * SL;                      // 16 * SL admm gap partials
+  double* sy = partG + 16 * SL;                         // SL * M staged next measurements
+  SlotState<SL>& ss = *reinterpret_cast<SlotState<SL>*>(sy + SL * M);
+  uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // SL * 256: row -> measurement index
+  uint8_t* sm = pos + SL * kMaxN;                       // SL * stage_mask_bytes(M) staged mask rows
+  const int cred = (SL == 32) ? col_of_reduced(lane) : col_of_reduced4(lane);
 
-  double p0[2][4][2], p1[2][4][2];
+  double p0[MAXRB][CB][2], p1[MAXRB][CB][2];
 #pragma unroll
-  for (int rb = 0; rb < 2; ++rb)
+  for (int rb = 0; rb < MAXRB; ++rb)
 #pragma unroll
-    for (int cb = 0; cb < 4; ++cb)
+    for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
       for (int i = 0; i < 2; ++i) p0[rb][cb][i] = p1[rb][cb][i] = 0.0;
-  if (threadIdx.x < kSlots) {
+  if (threadIdx.x < SL) {
     ss.status[threadIdx.x] = kEmpty;
     ss.retired[threadIdx.x] = 0;
     ss.need_pf[threadIdx.x] = 0;
@@ -262,14 +277,25 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     ss.nact[0] = ss.nact[1] = 0;
   }
   __syncthreads();
-  for (int s = w; s < kSlots; s += W) prefetch_slot<ALGO>(a, ss, sy, sm, s);
+  for (int s = w; s < SL; s += W) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
   const double* mat1 = (ALGO == kFista) ? a.fragT : a.fragS;
   const double* mat2 = (ALGO == kFista) ? a.fragS : a.fragT;
+  // A-fragment prefetch registers (the next GEMM's first k-steps)
   double2 af[4];
-  gemm_preload(nrb, mat1, rb0, KS, af);
+  double af16[4][4];
+  auto preload = [&](const double* m) {
+    if constexpr (SL == 32) gemm_preload(nrb, m, rb0, KS, af); else gemm_preload16(nrb, m, rb0, KS, af16);
+  };
+  double acc[MAXRB][CB][2];
+  auto gemm = [&](const double* m, const double* in) {
+    if constexpr (SL == 32) tile_gemm(nrb, m, rb0, in, KS, acc, af); else tile_gemm16(nrb, m, rb0, in, KS, acc, af16);
+  };
+  auto reduce = [&](const double (&v)[NV]) -> double {
+    if constexpr (SL == 32) return col_reduce8(v, lane); else return col_reduce4(v, lane);
+  };
+  preload(mat1);
 
-  double acc[2][4][2];
 #ifdef HCS_PHASES
   long long cph[16] = {0};
   cph[15] = clock64();
@@ -282,12 +308,12 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     // ---- slot phase: stop rule of the last iteration, refill, momentum ----
     // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
     // serial stop-rule / momentum code of a warp's slots runs side by side
-    for (int s0 = w; s0 < kSlots; s0 += 2 * W) {
+    for (int s0 = w; s0 < SL; s0 += 2 * W) {
       const int hl = lane & 15, s = s0 + (lane >> 4) * W;
-      const bool valid = s < kSlots;
+      const bool valid = s < SL;
       const bool was_active = valid && ss.status[s] == kActive;
-      double dd = (was_active && hl < W) ? partD[hl * kSlots + s] : 0.0;
-      double gg = (ALGO == kAdmm && was_active && hl < W) ? partG[hl * kSlots + s] : 0.0;
+      double dd = (was_active && hl < W) ? partD[hl * SL + s] : 0.0;
+      double gg = (ALGO == kAdmm && was_active && hl < W) ? partG[hl * SL + s] : 0.0;
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) {
         dd += __shfl_xor_sync(0xffffffffu, dd, o);
@@ -297,17 +323,17 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
         ss.retired[s] = 0;
         if (was_active) {
           if (ALGO == kFista) ss.t[s] = ss.tn[s];
-          finish_iteration(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
+          finish_iteration<SL>(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
         }
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int sk = s0 + k * W;
-        if (sk >= kSlots) break;
+        if (sk >= SL) break;
         if (ALGO == kAdmm && ss.retired[sk] && ss.rfail[sk])   // NumericalFailure: x = 0
           for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
-        if (ss.status[sk] != kActive) refill_slot<ALGO>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+        if (ss.status[sk] != kActive) refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
       }
       if (hl == 0 && valid) {
         if (ss.status[s] == kActive) {
@@ -330,16 +356,16 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     if (threadIdx.x == 0) ss.nact[par ^ 1] = 0;
     __syncthreads();
     CMARK(0);
-    for (int s = w; s < kSlots; s += W)
+    for (int s = w; s < SL; s += W)
       if (ss.need_pf[s]) {
         __syncwarp();
         if (lane == 0) ss.need_pf[s] = 0;
-        prefetch_slot<ALGO>(a, ss, sy, sm, s);
+        prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       }
 
     // ---- writeback of retired slots (element layout), fresh iterates -------
 #pragma unroll
-    for (int cb = 0; cb < 4; ++cb)
+    for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int s = acc_col(cb, i, lane);
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           const long long pid = ss.rpid[s];
           const bool fail = ss.rfail[s];
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
+          for (int rb = 0; rb < MAXRB; ++rb) {
             if (rb >= nrb) break;
             const int n = row0 + 8 * rb;
             if (ALGO == kFista && n < N) a.x_out[pid * N + n] = fail ? 0.0 : p0[rb][cb][i];
@@ -359,23 +385,23 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
     if (ss.nact[par] == 0) break;
     CMARK(1);
 
-    double part[8];
+    double part[NV];
     if (ALGO == kFista) {
       // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
-      tile_gemm(nrb, a.fragT, rb0, bufA, KS, acc, af);
+      gemm(a.fragT, bufA);
       __syncthreads();
       CMARK(2);
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb)
+      for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
           const double il = ss.inv_l[s], th = ss.thr[s], bn = ss.betan[s];
           bool bad = false;
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
+          for (int rb = 0; rb < MAXRB; ++rb) {
             if (rb >= nrb) break;
-            const int zi = in_idx(row0 + 8 * rb, s);
+            const int zi = slot_idx<SL>(row0 + 8 * rb, s);
             const double x = p0[rb][cb][i], z = bufB[zi];
             const double aux = __dsub_rn(z, __dmul_rn(il, acc[rb][cb][i]));   // solvers.py:183
             const double xn = soft(aux, th);                                    // solvers.py:185
@@ -386,22 +412,22 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           }
           if (bad) ss.flag[s] = 1;
         }
-      gemm_preload(nrb, mat2, rb0, KS, af);   // next GEMM's first k-steps
+      preload(mat2);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(3);
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
-      tile_gemm(nrb, a.fragS, rb0, bufA, KS, acc, af);
+      gemm(a.fragS, bufA);
       __syncthreads();
       CMARK(4);
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb)
+      for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
           const double bn = ss.betan[s];
           double dd = 0.0;
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
+          for (int rb = 0; rb < MAXRB; ++rb) {
             if (rb >= nrb) break;
             const int n = row0 + 8 * rb;
             const int pj = pos[s * kMaxN + n];
@@ -415,37 +441,37 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
               // next gradient input A z - y = -(1 + b) r + b r_prev
               g = (bn == 0.0) ? -rn : -(1.0 + bn) * rn + bn * ro;
             }
-            bufA[in_idx(n, s)] = g;
+            bufA[slot_idx<SL>(n, s)] = g;
           }
           part[2 * cb + i] = dd;
         }
-      partD[w * kSlots + cred] = col_reduce8(part, lane);
-      gemm_preload(nrb, mat1, rb0, KS, af);   // next GEMM's first k-steps
+      partD[w * SL + cred] = reduce(part);
+      preload(mat1);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(5);
     } else {
       // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
       //      residual y - A x = y - u'[mask] of this iteration's x ----------
-      tile_gemm(nrb, a.fragS, rb0, bufA, KS, acc, af);
+      gemm(a.fragS, bufA);
       CMARK(2);
       const double alpha = a.prm.alpha;
       // 1 / (d + alpha) for d = 0, 1 (Psi orthonormal: the factor's eigenvalues)
       const double inv0 = 1.0 / alpha, inv1 = 1.0 / (1.0 + alpha);
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb)
+      for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
           double dd = 0.0;
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
+          for (int rb = 0; rb < MAXRB; ++rb) {
             if (rb >= nrb) break;
             const int n = row0 + 8 * rb;
             const int pj = pos[s * kMaxN + n];
             const bool in_mask = pj != 0xFF;
             const double yh = in_mask ? ys[s * M + pj] : 0.0;
             const double up = (yh + alpha * acc[rb][cb][i]) * (in_mask ? inv1 : inv0);
-            bufB[in_idx(n, s)] = up;
+            bufB[slot_idx<SL>(n, s)] = up;
             if (in_mask) {
               const double rn = yh - up;
               const double d = rn - r[s * M + pj];
@@ -455,15 +481,15 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           }
           part[2 * cb + i] = dd;
         }
-      partD[w * kSlots + cred] = col_reduce8(part, lane);
-      gemm_preload(nrb, mat2, rb0, KS, af);   // next GEMM's first k-steps
+      partD[w * SL + cred] = reduce(part);
+      preload(mat2);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(3);
       // ---- GEMM 2: x = Psi^T u'; epilogue: shrink, dual update, gap --------
-      tile_gemm(nrb, a.fragT, rb0, bufB, KS, acc, af);
+      gemm(a.fragT, bufB);
       CMARK(4);
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb)
+      for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int s = acc_col(cb, i, lane);
@@ -473,7 +499,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           bool bad = false;
           double g2 = 0.0;
 #pragma unroll
-          for (int rb = 0; rb < 2; ++rb) {
+          for (int rb = 0; rb < MAXRB; ++rb) {
             if (rb >= nrb) break;
             const int n = row0 + 8 * rb;
             const double x = acc[rb][cb][i], wv = p1[rb][cb][i];
@@ -483,7 +509,7 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
             // it needs no registers between passes
             if (act && n < N) xo[n] = zn;
             p1[rb][cb][i] = wn;
-            bufA[in_idx(n, s)] = zn - wn;                                 // next GEMM 1 input
+            bufA[slot_idx<SL>(n, s)] = zn - wn;                           // next GEMM 1 input
             const double dg = x - zn;
             g2 += dg * dg;
             bad |= !isfinite(zn);
@@ -491,8 +517,8 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
           part[2 * cb + i] = g2;
           if (bad) ss.flag[s] = 1;
         }
-      partG[w * kSlots + cred] = col_reduce8(part, lane);
-      gemm_preload(nrb, mat1, rb0, KS, af);   // next GEMM's first k-steps
+      partG[w * SL + cred] = reduce(part);
+      preload(mat1);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(5);
     }
@@ -505,12 +531,13 @@ __global__ void __launch_bounds__(MAXT, 1) convex_kernel(ConvexArgs a) {
 
 // Fragment-order copies of Psi and Psi^T (layout of tile_gemm), and
 // u0 = Psi * (1/sqrt(N)) 1.  Row block rb's fragment for k-step ks, lane l is
-// Mat[8 rb + l/4][4 ks + l%4]; blocks owned in pairs by one warp (warp_rows)
-// are interleaved as double2.
+// Mat[8 rb + l/4][4 ks + l%4]; with `interleave` (the 32-slot engine) blocks
+// owned in pairs by one warp (warp_rows) are interleaved as double2, else the
+// order is plain (the 16-slot engine, tile_gemm16).
 __global__ void prep_basis_kernel(const double* __restrict__ basis, int N, int Np, double* fragS, double* fragT,
-                                  double* u0) {
+                                  double* u0, int interleave) {
   const int KS = Np >> 2, RB = Np >> 3;
-  const int nd = RB > 16 ? RB - 16 : 0;
+  const int nd = (interleave && RB > 16) ? RB - 16 : 0;
   const long long total = (long long)RB * KS * 32;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -554,35 +581,56 @@ cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, co
 }
 
 cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
-                              cudaStream_t stream) {
-  prep_basis_kernel<<<64, 256, 0, stream>>>(basis, N, Np, fragS, fragT, u0);
+                              int slots, cudaStream_t stream) {
+  prep_basis_kernel<<<64, 256, 0, stream>>>(basis, N, Np, fragS, fragT, u0, slots == 32 ? 1 : 0);
   return cudaGetLastError();
 }
 
-size_t convex_smem_bytes(int algo, int Np, int M) {
+size_t convex_smem_bytes(int algo, int Np, int M, int slots) {
   (void)algo;
-  size_t b = sizeof(double) * (size_t)Np * kSlots * 2;               // bufA, bufB
-  b += sizeof(double) * (size_t)kSlots * M * 2;                      // ys, r
-  b += sizeof(double) * 2 * 16 * kSlots;                             // partD, partG
-  b += sizeof(double) * (size_t)kSlots * M;                          // sy
-  b += sizeof(SlotState);
-  b += (size_t)kSlots * kMaxN;                                       // pos
-  b += (size_t)kSlots * stage_mask_bytes(M);                         // sm
+  const size_t sl = (size_t)slots;
+  size_t b = sizeof(double) * (size_t)Np * sl * 2;                   // bufA, bufB
+  b += sizeof(double) * sl * M * 2;                                  // ys, r
+  b += sizeof(double) * 2 * 16 * sl;                                 // partD, partG
+  b += sizeof(double) * sl * M;                                      // sy
+  b += slots == 32 ? sizeof(SlotState<32>) : sizeof(SlotState<16>);
+  b += sl * kMaxN;                                                   // pos
+  b += sl * stage_mask_bytes(M);                                     // sm
   return (b + 15) & ~(size_t)15;
 }
 
-template <int ALGO, int MAXT>
+// Slot engine variant for (Np, M): 32 slots x one CTA per SM (default).  The
+// 16-slot x two-CTAs-per-SM engine (HCS_CONVEX_SLOTS=16, experiments) runs
+// the two CTAs out of phase, but on B200 the FP64 epilogue / slot-phase
+// arithmetic shares the FP64 datapath with DMMA, so it queues behind the other
+// CTA's tensor work instead of overlapping it: measured 15% slower (FISTA
+// 62.6 -> 73.2 ms, ADMM 103.7 -> 120.6 ms on 100k Salinas pixels;
+// epilogue cycles x5.6 per CTA; profiles/convex_slots_ab_r01.txt).
+int convex_slots(int algo, int Np, int M) {
+  int want = 32;
+  if (const char* ov = getenv("HCS_CONVEX_SLOTS")) want = atoi(ov) == 16 ? 16 : 32;
+  if (want == 16 && 2 * (convex_smem_bytes(algo, Np, M, 16) + 1024) > 228 * 1024) want = 32;
+  return want;
+}
+
+template <int ALGO, int SL, int MAXT, int MINB>
 static cudaError_t launch_convex_t(const ConvexArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, SL, MAXT, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  convex_kernel<ALGO, MAXT><<<grid, 32 * engine_warps(args.Np), smem, stream>>>(args);
+  const int warps = SL == 32 ? engine_warps(args.Np) : engine_warps16(args.Np);
+  convex_kernel<ALGO, SL, MAXT, MINB><<<grid, 32 * warps, smem, stream>>>(args);
   return cudaGetLastError();
 }
 
-cudaError_t launch_convex(int algo, const ConvexArgs& args, int grid, cudaStream_t stream) {
-  const size_t smem = convex_smem_bytes(algo, args.Np, args.M);
-  if (algo == kFista) return launch_convex_t<kFista, 512>(args, grid, smem, stream);
-  return launch_convex_t<kAdmm, 512>(args, grid, smem, stream);
+cudaError_t launch_convex(int algo, const ConvexArgs& args, int slots, int grid, cudaStream_t stream) {
+  const size_t smem = convex_smem_bytes(algo, args.Np, args.M, slots);
+  if (slots == 32) {
+    if (algo == kFista) return launch_convex_t<kFista, 32, 512, 1>(args, grid, smem, stream);
+    return launch_convex_t<kAdmm, 32, 512, 1>(args, grid, smem, stream);
+  }
+  if (algo == kFista) return launch_convex_t<kFista, 16, 256, 2>(args, grid, smem, stream);
+  return launch_convex_t<kAdmm, 16, 256, 2>(args, grid, smem, stream);
 }
 
 }  // namespace hcs

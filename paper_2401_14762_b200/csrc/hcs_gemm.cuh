@@ -205,4 +205,104 @@ __device__ __forceinline__ int col_of_reduced(int lane) {
   return 8 * (2 * ((lane >> 2) & 1) + ((lane >> 3) & 1)) + 2 * (lane & 3) + ((lane >> 4) & 1);
 }
 
+// ---------------------------------------------------------------------------
+// Half-width engine (two CTAs per SM, 16 slots, 8 warps): the same GEMM with
+// CB = 2 column blocks and up to 4 row blocks per warp, so that the two CTAs
+// of an SM run out of phase and one CTA's epilogue / slot phase overlaps the
+// other's DMMA work.  The matrix is read in the plain fragment order (row
+// block rb, k-step ks at (rb KS + ks) * 32, prep_basis with interleave off);
+// In holds 16 columns: in_idx16.
+constexpr int kSlots16 = 16;
+
+__device__ __forceinline__ int in_idx16(int k, int s) {
+  return (((k >> 2) * 2 + (s >> 3)) << 5) + ((s & 7) << 2) + (k & 3);
+}
+
+// Contiguous balanced row-block map over W warps: warps w < RB % W own one
+// more block.  With W = 8 the warp pairs (w, w + 4) share an SM sub-partition,
+// so N = 224 (RB = 28) puts 4 + 3 = 7 blocks on each.
+__device__ __forceinline__ void warp_rows16(int RB, int W, int w, int& rb0, int& nrb) {
+  const int base = RB / W, extra = RB % W;
+  nrb = base + (w < extra ? 1 : 0);
+  rb0 = w * base + (w < extra ? w : extra);
+}
+__host__ __device__ __forceinline__ int engine_warps16(int Np) { return (Np >> 3) < 8 ? (Np >> 3) : 8; }
+
+template <int NRB>
+__device__ __forceinline__ void gemm_preload16(const double* __restrict__ frag, int rb0, int KS, double (&a)[4][4]) {
+  const double* fa = frag + (size_t)rb0 * KS * 32 + (threadIdx.x & 31);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int rb = 0; rb < NRB; ++rb) a[i][rb] = __ldg(fa + ((size_t)rb * KS + i) * 32);
+}
+__device__ __forceinline__ void gemm_preload16(int nrb, const double* frag, int rb0, int KS, double (&a)[4][4]) {
+  switch (nrb) {
+    case 4: gemm_preload16<4>(frag, rb0, KS, a); break;
+    case 3: gemm_preload16<3>(frag, rb0, KS, a); break;
+    case 2: gemm_preload16<2>(frag, rb0, KS, a); break;
+    default: gemm_preload16<1>(frag, rb0, KS, a); break;
+  }
+}
+
+// acc[rb][cb] = Mat(row block rb0 + rb) * In(column block cb), rb < NRB, cb < 2;
+// a holds the gemm_preload16 fragments (k-steps 0..3) on entry; each is
+// reloaded 4 k-steps ahead right after its last use.
+template <int NRB>
+__device__ __forceinline__ void tile_gemm16(const double* __restrict__ frag, int rb0, const double* In, int KS,
+                                            double (&acc)[4][2][2], double (&a)[4][4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+  const double* fa = frag + (size_t)rb0 * KS * 32 + lane;
+  for (int ks0 = 0; ks0 < KS; ks0 += 4) {
+    const bool more = ks0 + 4 < KS;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double* b = In + ((ks0 + i) << 6) + lane;
+      const double b0 = b[0], b1 = b[32];
+#pragma unroll
+      for (int rb = 0; rb < NRB; ++rb) {
+        dmma(acc[rb][0], a[i][rb], b0);
+        dmma(acc[rb][1], a[i][rb], b1);
+      }
+      if (more) {
+#pragma unroll
+        for (int rb = 0; rb < NRB; ++rb) a[i][rb] = __ldg(fa + ((size_t)rb * KS + ks0 + 4 + i) * 32);
+      }
+    }
+  }
+}
+__device__ __forceinline__ void tile_gemm16(int nrb, const double* frag, int rb0, const double* In, int KS,
+                                            double (&acc)[4][2][2], double (&a)[4][4]) {
+  switch (nrb) {
+    case 4: tile_gemm16<4>(frag, rb0, In, KS, acc, a); break;
+    case 3: tile_gemm16<3>(frag, rb0, In, KS, acc, a); break;
+    case 2: tile_gemm16<2>(frag, rb0, In, KS, acc, a); break;
+    default: tile_gemm16<1>(frag, rb0, In, KS, acc, a); break;
+  }
+}
+
+// Column sums for 16 slot columns: v[2 cb + i] is this lane's value for
+// column 8 cb + 2 (lane & 3) + i.  Two transpose-and-add stages (lane bits 2,
+// 3) and one plain stage (bit 4) leave the full 8-row sum of column
+// col_of_reduced4(lane) in this lane (lanes l and l ^ 16 hold the same column).
+__device__ __forceinline__ double col_reduce4(const double (&v)[4], int lane) {
+  const bool b = (lane >> 2) & 1, c = (lane >> 3) & 1;
+  double u[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = b ? v[k] : v[k + 2], keep = b ? v[k + 2] : v[k];
+    u[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const double send = c ? u[0] : u[1], keep = c ? u[1] : u[0];
+  double q = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  return q + __shfl_xor_sync(0xffffffffu, q, 16);
+}
+__device__ __forceinline__ int col_of_reduced4(int lane) {
+  return 8 * ((lane >> 2) & 1) + 2 * (lane & 3) + ((lane >> 3) & 1);
+}
+
 }  // namespace hcs

@@ -38,12 +38,13 @@ struct GreedyArgs {
 };
 
 // hcs_convex.cu
-cudaError_t launch_convex(int algo, const ConvexArgs& args, int grid, cudaStream_t stream);
-size_t convex_smem_bytes(int algo, int Np, int M);
+cudaError_t launch_convex(int algo, const ConvexArgs& args, int slots, int grid, cudaStream_t stream);
+size_t convex_smem_bytes(int algo, int Np, int M, int slots);
+int convex_slots(int algo, int Np, int M);
 cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
                                      int sms, cudaStream_t stream);
 cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
-                              cudaStream_t stream);
+                              int slots, cudaStream_t stream);
 // hcs_greedy.cu
 cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream);
 size_t greedy_smem_bytes(int M, int kalloc);

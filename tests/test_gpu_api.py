@@ -307,3 +307,30 @@ def test_chunked_pipeline_reports_nonfinite_from_any_chunk():
     with pytest.raises(ValueError):
         hcs.recover_cube(meas, d, hcs.SolverConfig(kappa=22, time_limit=None), "gomp",
                          out=np.empty((6, 10, 153)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo,params", [("fista", dict(lam=0.1)), ("admm", dict(lam=0.1)), ("admm", dict(lam=100.0))])
+def test_convex_slot_engines_agree(monkeypatch, algo, params):
+    """The 16-slot x two-CTAs-per-SM engine (HCS_CONVEX_SLOTS=16, kept for
+    experiments) performs the same per-element arithmetic in the same order as
+    the default 32-slot engine; only the residual-delta partial sums are summed
+    over a different warp split (8 vs 16 warps), so delta may differ in the
+    last bits: iterations and x must agree exactly, delta to 1e-12."""
+    import torch
+    from paper_2401_14762_b200 import synth
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    c = synth.generate(6, 50, 224, seed=21)
+    dev = torch.device("cuda")
+    args = (torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev), torch.as_tensor(c.basis, device=dev),
+            SolverConfig(time_limit=None, max_iter=5000, **params))
+    outs = []
+    for slots in ("32", "16"):
+        monkeypatch.setenv("HCS_CONVEX_SLOTS", slots)
+        b = solve_batch(algo, *args)
+        torch.cuda.synchronize()
+        outs.append((b.x.cpu().numpy(), b.iterations.cpu().numpy(), b.final_delta.cpu().numpy()))
+    (x32, it32, d32), (x16, it16, d16) = outs
+    assert np.array_equal(it32, it16), f"{int((it32 != it16).sum())} iteration mismatches"
+    assert np.max(np.abs(x32 - x16)) <= 1e-13 * max(np.max(np.abs(x32)), 1e-300), np.max(np.abs(x32 - x16))
+    assert np.allclose(d32, d16, rtol=1e-12, atol=0)

@@ -1,0 +1,135 @@
+// Latency probe of the CSNE 8x8 diagonal-tile factorisation (hcs_ls_csne.cuh):
+// clock64 around consecutive csne_diag_factor calls by one warp on an SPD tile.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -I paper_2401_14762_b200/csrc -o tools/diag_probe tools/diag_probe.cu
+#include <cstdio>
+#include "hcs_ls_csne.cuh"
+
+namespace hcs {
+// Warp 0: Cholesky of the 8 x 8 diagonal tile kb, reciprocal pivots into dinv,
+// and the inverse L_kk^-1 stored transposed in the tile's strictly upper part.
+// A non-positive pivot clears sc.flag.  Every lane factors the whole tile
+// redundantly in registers (no shuffles on the serial pivot chain: the
+// column-c update needs L_kc of every row, which a row-per-lane layout has to
+// shuffle in one k at a time); lane ii < 8 then stores row ii and computes
+// column ii of the inverse from registers.  The operation sequence per element
+// is the row-per-lane one's, so the results are bitwise the same.
+static __device__ __noinline__ void csne_diag_factor_v2(double* G, const CsneScratch sc, int K, int kb) {
+  const int lane = threadIdx.x & 31;
+  const int o = 8 * kb;
+  const int w = K - o < 8 ? K - o : 8;
+  const int base = gtile(kb, kb);
+  double L[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) L[i][k] = G[base + k * 8 + i];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < w) {
+      const double d = L[c][c];
+      ok = ok && d > 0.0;
+      const double rs = rsqrt(d);
+      L[c][c] = d * rs;                       // L_cc = sqrt(d)
+#pragma unroll
+      for (int i = c + 1; i < 8; ++i) L[i][c] *= rs;
+#pragma unroll
+      for (int k = c + 1; k < 8; ++k)
+#pragma unroll
+        for (int i = k; i < 8; ++i) L[i][k] -= L[i][c] * L[k][c];
+    }
+  }
+  double dinv[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) dinv[m] = (m < w) ? 1.0 / L[m][m] : 0.0;
+  const int ii = lane;
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i == ii) {
+#pragma unroll
+        for (int k = 0; k <= i; ++k) G[base + k * 8 + i] = L[i][k];   // lower part incl. diagonal
+        sc.dinv[o + i] = dinv[i];
+      }
+  }
+  if (lane == 0 && !ok) sc.flag[0] = 0;
+  __syncwarp();
+  // inverse of L_kk (lower), column jj per lane, from the registers
+  if (lane < 8) {
+    const int jj = lane;
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      double v = 0.0;
+      if (m == jj) {
+        v = dinv[m];
+      } else if (m > jj && m < w) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < m; ++p)
+          if (p >= jj) acc += L[m][p] * x[p];
+        v = -acc * dinv[m];
+      }
+      x[m] = v;
+    }
+#pragma unroll
+    for (int m = 1; m < 8; ++m)
+      if (m > jj) G[base + m * 8 + jj] = x[m];         // Linv[m][jj] at (row jj, col m)
+  }
+  __syncwarp();
+}
+
+}  // namespace hcs
+
+template <int V>
+__global__ void probe(long long* out, int reps, double* res) {
+  __shared__ double G[16 * 68];
+  __shared__ double dinv[16], c[16], r[128], red[16];
+  __shared__ int flag;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < 16 * 68; i += 32) G[i] = 0.0;
+  __syncwarp();
+  if (lane < 8)
+    for (int k = 0; k < 8; ++k) G[k * 8 + lane] = (k == lane ? 10.0 : 0.0) + 1.0 / (1 + k + lane);
+  __syncwarp();
+  hcs::CsneScratch sc{G, dinv, c, r, red, &flag};
+  for (int t = 0; t < reps; ++t) {
+    if (lane < 8)
+      for (int k = 0; k < 8; ++k) G[k * 8 + lane] = (k == lane ? 10.0 : 0.0) + 1.0 / (1 + k + lane);
+    __syncwarp();
+    long long t0 = clock64();
+    if (V == 1) hcs::csne_diag_factor(G, sc, 8, 0); else if (V == 2) hcs::csne_diag_factor_v2(G, sc, 8, 0); else if (V == 3) hcs::csne_diag_factor(G, sc, 6, 0); else hcs::csne_diag_factor_v2(G, sc, 6, 0);
+    __syncwarp();
+    long long t1 = clock64();
+    if (lane == 0) out[t] = t1 - t0;
+  }
+  if (lane == 0) out[reps] = (long long)(dinv[3] * 1e6);
+  for (int i = lane; i < 64; i += 32) res[i] = G[i];
+  if (lane < 8) res[64 + lane] = dinv[lane];
+}
+
+int main() {
+  long long* d;
+  double* r;
+  cudaMalloc(&d, 64 * sizeof(long long));
+  cudaMalloc(&r, 4 * 80 * sizeof(double));
+  long long h[64];
+  double hr[4][80];
+  for (int v = 1; v <= 4; ++v) {
+    for (int launch = 0; launch < 2; ++launch) {
+      if (v == 1) probe<1><<<1, 32>>>(d, 8, r + 0);
+      if (v == 2) probe<2><<<1, 32>>>(d, 8, r + 80);
+      if (v == 3) probe<3><<<1, 32>>>(d, 8, r + 160);
+      if (v == 4) probe<4><<<1, 32>>>(d, 8, r + 240);
+      cudaMemcpy(h, d, 9 * sizeof(long long), cudaMemcpyDeviceToHost);
+      printf("variant %d launch %d cycles per call:", v, launch);
+      for (int i = 0; i < 8; ++i) printf(" %lld", h[i]);
+      printf("\n");
+    }
+  }
+  cudaMemcpy(hr, r, sizeof(hr), cudaMemcpyDeviceToHost);
+  int diff = 0, diff6 = 0;
+  for (int i = 0; i < 72; ++i) { diff += hr[0][i] != hr[1][i]; diff6 += hr[2][i] != hr[3][i]; }
+  printf("bitwise differences old vs new: K=8 %d, K=6 %d (of 72)\n", diff, diff6);
+  return 0;
+}
