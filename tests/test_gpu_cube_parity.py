@@ -14,6 +14,7 @@ profiles/cube_parity_r01.jsonl.)
 """
 
 import math
+import multiprocessing
 import os
 from concurrent.futures import ProcessPoolExecutor
 
@@ -43,7 +44,9 @@ CASES = [
 @pytest.fixture(scope="module")
 def pool():
     cores = max(1, len(os.sched_getaffinity(0)))
-    with ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas) as p:
+    # forkserver: the workers must not inherit this process's CUDA context
+    ctx = multiprocessing.get_context("forkserver")
+    with ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas, mp_context=ctx) as p:
         yield p, cores
 
 

@@ -18,6 +18,7 @@ be traced to them.  Diagnostics only: the oracle is test infrastructure.
 
 import argparse
 import json
+import multiprocessing
 import os
 import sys
 import time
@@ -114,7 +115,8 @@ def main():
     only = set(args.only.split(",")) if args.only else None
     dev = torch.device("cuda")
     cubes = {}
-    pool = ProcessPoolExecutor(max_workers=args.jobs, initializer=oc.single_thread_blas)
+    pool = ProcessPoolExecutor(max_workers=args.jobs, initializer=oc.single_thread_blas,
+                               mp_context=multiprocessing.get_context("forkserver"))
     for tag, cube_name, algo, params, cap in CASES:
         if only and tag not in only:
             continue

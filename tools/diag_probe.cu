@@ -79,7 +79,174 @@ static __device__ __noinline__ void csne_diag_factor_v2(double* G, const CsneScr
   __syncwarp();
 }
 
+// Warp 0: Cholesky of the 8 x 8 diagonal tile kb, reciprocal pivots into dinv,
+// and the inverse L_kk^-1 stored transposed in the tile's strictly upper part.
+// A non-positive pivot clears sc.flag.  Every lane factors the whole tile
+// redundantly in registers (no shuffles on the serial pivot chain: the
+// column-c update needs L_kc of every row, which a row-per-lane layout has to
+// shuffle in one k at a time); lane ii < 8 then stores row ii and computes
+// column ii of the inverse from registers.  The operation sequence per element
+// is the row-per-lane one's, so the results are bitwise the same.
+static __device__ __noinline__ void csne_diag_factor_v3(double* G, const CsneScratch sc, int K, int kb, long long* tm) {
+  long long c0 = clock64();
+  const int lane = threadIdx.x & 31;
+  const int o = 8 * kb;
+  const int w = K - o < 8 ? K - o : 8;
+  const int base = gtile(kb, kb);
+  double L[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) L[i][k] = G[base + k * 8 + i];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < w) {
+      const double d = L[c][c];
+      ok = ok && d > 0.0;
+      const double rs = rsqrt(d);
+      L[c][c] = d * rs;                       // L_cc = sqrt(d)
+#pragma unroll
+      for (int i = c + 1; i < 8; ++i) L[i][c] *= rs;
+#pragma unroll
+      for (int k = c + 1; k < 8; ++k)
+#pragma unroll
+        for (int i = k; i < 8; ++i) L[i][k] -= L[i][c] * L[k][c];
+    }
+  }
+  long long c1 = clock64();
+  double dinv[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) dinv[m] = (m < w) ? 1.0 / L[m][m] : 0.0;
+  long long c2 = clock64();
+  const int ii = lane;
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i == ii) {
+#pragma unroll
+        for (int k = 0; k <= i; ++k) G[base + k * 8 + i] = L[i][k];   // lower part incl. diagonal
+        sc.dinv[o + i] = dinv[i];
+      }
+  }
+  if (lane == 0 && !ok) sc.flag[0] = 0;
+  __syncwarp();
+  long long c3 = clock64();
+  // inverse of L_kk (lower), column jj per lane, from the registers
+  if (lane < 8) {
+    const int jj = lane;
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      double v = 0.0;
+      if (m == jj) {
+        v = dinv[m];
+      } else if (m > jj && m < w) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = 0; p < m; ++p)
+          if (p >= jj) acc += L[m][p] * x[p];
+        v = -acc * dinv[m];
+      }
+      x[m] = v;
+    }
+#pragma unroll
+    for (int m = 1; m < 8; ++m)
+      if (m > jj) G[base + m * 8 + jj] = x[m];         // Linv[m][jj] at (row jj, col m)
+  }
+  __syncwarp();
+  long long c4 = clock64();
+  if (lane == 0) { tm[0] = c1 - c0; tm[1] = c2 - c1; tm[2] = c3 - c2; tm[3] = c4 - c3; }
+}
+// Warp 0: Cholesky of the 8 x 8 diagonal tile kb, reciprocal pivots into dinv,
+// and the inverse L_kk^-1 stored transposed in the tile's strictly upper part.
+// A non-positive pivot clears sc.flag.  Every lane factors and inverts the
+// whole tile redundantly in registers, so the serial pivot chain has no
+// shuffles and every store has a compile-time register and address (all
+// lanes store the same value: no lane-dependent selects or divergent store
+// branches).  The inverse is formed in place, column by column: column j
+// needs L[m][p] for p >= j only, so Linv[m][j] may overwrite L[m][j] in
+// increasing m.  Per element the operation sequence is the row-per-lane /
+// column-per-lane one's, so the results are bitwise the same.
+static __device__ __noinline__ void csne_diag_factor_v4(double* G, const CsneScratch sc, int K, int kb) {
+  const int o = 8 * kb;
+  const int w = K - o < 8 ? K - o : 8;
+  double* T = G + gtile(kb, kb);
+  double L[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) L[i][k] = T[k * 8 + i];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < w) {
+      const double d = L[c][c];
+      ok = ok && d > 0.0;
+      const double rs = rsqrt(d);
+      L[c][c] = d * rs;                       // L_cc = sqrt(d)
+#pragma unroll
+      for (int i = c + 1; i < 8; ++i) L[i][c] *= rs;
+#pragma unroll
+      for (int k = c + 1; k < 8; ++k)
+#pragma unroll
+        for (int i = k; i < 8; ++i) L[i][k] -= L[i][c] * L[k][c];
+    }
+  }
+  double dinv[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) dinv[m] = (m < w) ? 1.0 / L[m][m] : 0.0;
+  // lower part incl. the diagonal, and the reciprocal pivots
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) T[k * 8 + i] = L[i][k];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) sc.dinv[o + m] = dinv[m];
+  if (!ok && (threadIdx.x & 31) == 0) sc.flag[0] = 0;
+  // inverse (strictly lower part), in place: Linv[m][j] = -(sum_{j<=p<m} L[m][p] Linv[p][j]) / L[m][m]
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    double x[8];
+    x[j] = dinv[j];
+#pragma unroll
+    for (int m = j + 1; m < 8; ++m) {
+      double v = 0.0;
+      if (m < w) {
+        double acc = 0.0;
+#pragma unroll
+        for (int p = j; p < m; ++p) acc += L[m][p] * x[p];
+        v = -acc * dinv[m];
+      }
+      x[m] = v;
+    }
+#pragma unroll
+    for (int m = j + 1; m < 8; ++m) L[m][j] = x[m];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 7; ++j)
+#pragma unroll
+    for (int m = j + 1; m < 8; ++m) T[m * 8 + j] = L[m][j];   // Linv[m][j] at (row j, col m)
+  __syncwarp();
+}
 }  // namespace hcs
+
+__global__ void probe_parts(long long* tm) {
+  __shared__ double G[16 * 68];
+  __shared__ double dinv[16], c[16], r[128], red[16];
+  __shared__ int flag;
+  const int lane = threadIdx.x;
+  hcs::CsneScratch sc{G, dinv, c, r, red, &flag};
+  for (int t = 0; t < 3; ++t) {
+    for (int i = lane; i < 16 * 68; i += 32) G[i] = 0.0;
+    __syncwarp();
+    if (lane < 8)
+      for (int k = 0; k < 8; ++k) G[k * 8 + lane] = (k == lane ? 10.0 : 0.0) + 1.0 / (1 + k + lane);
+    __syncwarp();
+    hcs::csne_diag_factor_v3(G, sc, 8, 0, tm);
+  }
+}
 
 template <int V>
 __global__ void probe(long long* out, int reps, double* res) {
@@ -98,7 +265,7 @@ __global__ void probe(long long* out, int reps, double* res) {
       for (int k = 0; k < 8; ++k) G[k * 8 + lane] = (k == lane ? 10.0 : 0.0) + 1.0 / (1 + k + lane);
     __syncwarp();
     long long t0 = clock64();
-    if (V == 1) hcs::csne_diag_factor(G, sc, 8, 0); else if (V == 2) hcs::csne_diag_factor_v2(G, sc, 8, 0); else if (V == 3) hcs::csne_diag_factor(G, sc, 6, 0); else hcs::csne_diag_factor_v2(G, sc, 6, 0);
+    if (V == 1) hcs::csne_diag_factor(G, sc, 8, 0); else if (V == 2) hcs::csne_diag_factor_v4(G, sc, 8, 0); else if (V == 3) hcs::csne_diag_factor(G, sc, 6, 0); else hcs::csne_diag_factor_v4(G, sc, 6, 0);
     __syncwarp();
     long long t1 = clock64();
     if (lane == 0) out[t] = t1 - t0;
@@ -130,6 +297,12 @@ int main() {
   cudaMemcpy(hr, r, sizeof(hr), cudaMemcpyDeviceToHost);
   int diff = 0, diff6 = 0;
   for (int i = 0; i < 72; ++i) { diff += hr[0][i] != hr[1][i]; diff6 += hr[2][i] != hr[3][i]; }
+  {
+    long long* tm; cudaMalloc(&tm, 8 * sizeof(long long));
+    probe_parts<<<1, 32>>>(tm);
+    long long ht[4]; cudaMemcpy(ht, tm, sizeof(ht), cudaMemcpyDeviceToHost);
+    printf("v2 parts (cycles): cholesky %lld, 8 reciprocals %lld, stores %lld, inverse+stores %lld\n", ht[0], ht[1], ht[2], ht[3]);
+  }
   printf("bitwise differences old vs new: K=8 %d, K=6 %d (of 72)\n", diff, diff6);
   return 0;
 }
