@@ -416,7 +416,7 @@ def _recover_host(algorithm, y_host, dictionary, config, x_host, chunk_pixels, s
         else:
             if dictionary.masks.shape[0] != P:
                 raise ValueError("per-pixel masks do not match the cube")
-            mask_src = torch.from_numpy(np.ascontiguousarray(dictionary.masks))
+            mask_src = dictionary.pinned_masks()
     ready = torch.cuda.Event()
     ready.record(main)
     for s in (s_in, s_c0, s_c1, s_out):

@@ -252,6 +252,17 @@ class Dictionary:
         return cls(basis=b, masks=masks)
 
     # ---- device residency ----------------------------------------------------
+    def pinned_masks(self):
+        """Per-pixel masks as a pinned host tensor (pinned once, cached): the
+        host pipeline of recover_cube copies them to the device every call
+        with asynchronous DMA instead of a staged pageable copy."""
+        import torch
+        hit = self._device.get("pinned")
+        if hit is None:
+            hit = torch.from_numpy(np.ascontiguousarray(self.masks)).pin_memory()
+            self._device["pinned"] = hit
+        return hit
+
     def device_arrays(self, device, n_pixels):
         """(basis, masks) as CUDA tensors; masks broadcast to n_pixels rows."""
         import torch
@@ -266,7 +277,9 @@ class Dictionary:
                     raise ValueError("per-pixel masks do not match the number of pixels")
                 masks = torch.as_tensor(self.masks, device=device)
             hit = (basis, masks)
-            self._device = {key: hit}
+            # one device copy at a time (the pinned host copy stays)
+            self._device = {k: v for k, v in self._device.items() if k == "pinned"}
+            self._device[key] = hit
         return hit
 
 
