@@ -156,16 +156,20 @@ __device__ __forceinline__ void csne_tile_update(double* G, int bi, int bj, int 
 // Warp 0: Cholesky of the 8 x 8 diagonal tile kb (lane ii < 8 holds row ii),
 // reciprocal pivots into dinv, and the inverse L_kk^-1 (column jj per lane)
 // stored transposed in the tile's strictly upper part.  A non-positive pivot
-// clears sc.flag.
+// clears sc.flag.  Branch-free: lane-dependent conditions are selects and
+// predicated stores, and the inverse reads the tile with lane-uniform
+// (broadcast) loads issued ahead of its dependency chain; column jj of the
+// inverse is zero above the diagonal, so the terms p < jj of its sums add
+// exact zeros and need no predicate.
 static __device__ __noinline__ void csne_diag_factor(double* G, const CsneScratch& sc, int K, int kb) {
   const int lane = threadIdx.x & 31;
   const int o = 8 * kb;
   const int w = K - o < 8 ? K - o : 8;
-  const int base = gtile(kb, kb);
+  double* T = G + gtile(kb, kb);
   double row[8];
   const int ii = lane & 7;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) row[k] = G[base + k * 8 + ii];
+  for (int k = 0; k < 8; ++k) row[k] = T[k * 8 + ii];
   bool ok = true;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -173,52 +177,53 @@ static __device__ __noinline__ void csne_diag_factor(double* G, const CsneScratc
       const double d = __shfl_sync(0xffffffffu, row[c], c);
       ok = ok && d > 0.0;
       const double rs = rsqrt(d);
-      if (ii == c) row[c] = d * rs;            // L_cc = sqrt(d)
-      if (ii > c) row[c] *= rs;                // L_ic
+      row[c] = (ii == c) ? d * rs : (ii > c ? row[c] * rs : row[c]);   // L_cc = sqrt(d), L_ic
 #pragma unroll
       for (int k = 1; k < 8; ++k) {
         if (k > c) {
           const double lkc = __shfl_sync(0xffffffffu, row[c], k);   // L_kc from lane k
-          if (ii >= k) row[k] -= row[c] * lkc;
+          const double upd = row[k] - row[c] * lkc;
+          row[k] = (ii >= k) ? upd : row[k];
         }
       }
     }
   }
-  double rii = 1.0;
+  double rii = row[0];
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    if (k == ii) rii = row[k];
+  for (int k = 1; k < 8; ++k) rii = (k == ii) ? row[k] : rii;
   const double dii = (ii < w) ? 1.0 / rii : 0.0;
   if (lane < 8) {
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (k <= ii) G[base + k * 8 + ii] = row[k];    // lower part incl. diagonal
+      if (k <= ii) T[k * 8 + ii] = row[k];    // lower part incl. diagonal
     sc.dinv[o + ii] = dii;
   }
   if (lane == 0 && !ok) sc.flag[0] = 0;
   __syncwarp();
   // inverse of L_kk (lower), column jj per lane
+  double Lm[8][8], dv[8];
+#pragma unroll
+  for (int m = 1; m < 8; ++m) {
+    dv[m] = sc.dinv[o + m];
+#pragma unroll
+    for (int p = 0; p < m; ++p) Lm[m][p] = T[p * 8 + m];
+  }
+  const int jj = ii;
+  double x[8];
+  x[0] = (jj == 0) ? dii : 0.0;
+#pragma unroll
+  for (int m = 1; m < 8; ++m) {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p < m; ++p) acc += Lm[m][p] * x[p];
+    const double v = -acc * dv[m];
+    x[m] = (m == jj) ? dii : ((m > jj && m < w) ? v : 0.0);
+  }
+  __syncwarp();
   if (lane < 8) {
-    const int jj = lane;
-    double x[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      double v = 0.0;
-      if (m == jj) {
-        v = dii;
-      } else if (m > jj && m < w) {
-        double acc = 0.0;
-#pragma unroll
-        for (int p = 0; p < 7; ++p)
-          if (p >= jj && p < m) acc += G[base + p * 8 + m] * x[p];
-        v = -acc * sc.dinv[o + m];
-      }
-      x[m] = v;
-    }
-    __syncwarp(0xffu);
 #pragma unroll
     for (int m = 1; m < 8; ++m)
-      if (m > jj) G[base + m * 8 + jj] = x[m];         // Linv[m][jj] at (row jj, col m)
+      if (m > jj) T[m * 8 + jj] = x[m];         // Linv[m][jj] at (row jj, col m)
   }
   __syncwarp();
 }
