@@ -53,6 +53,16 @@ CASES = [
     ("cfg5t0", "salinas", "admm", dict(lam=100.0, alpha=1.8), 5000),
     ("cfg5t0", "salinas", "admm", dict(lam=0.1, alpha=1.8), 5000),
 ]
+# BASELINE config 5 at its full size (1,777,664 px): the solvers the oracle finishes in minutes
+CASES += [
+    ("cfg5", "scaling", "gomp", dict(kappa=27, atoms_per_iter=5), None),
+    ("cfg5", "scaling", "gomp", dict(kappa=33, atoms_per_iter=6), None),
+    ("cfg5", "scaling", "biht", dict(kappa=27, mu=0.1), 2000),
+    ("cfg5", "scaling", "biht", dict(kappa=33, mu=0.1), 2000),
+    ("cfg5", "scaling", "cosamp", dict(kappa=33), 2000),
+    ("cfg5", "scaling", "fista", dict(lam=100.0), 5000),
+    ("cfg5", "scaling", "fista", dict(lam=0.1), 5000),
+]
 SLOW = {("salinas", "admm", 0.1)}
 
 
@@ -138,7 +148,8 @@ def main():
         gfail = b.failed_at.cpu().numpy()
         ocfg = oc.OracleConfig(max_iter=cap or 0, **params)
         t = time.perf_counter()
-        ref = oc.solve_cube(algo, c.basis, c.y, c.masks, ocfg, jobs=args.jobs, pool=pool, chunk=256)
+        ref = oc.solve_cube(algo, c.basis, c.y, c.masks, ocfg, jobs=args.jobs, pool=pool,
+                            chunk=256 if c.n_pixels < 200000 else 2048)
         t_or = time.perf_counter() - t
         P = c.n_pixels
         nr = np.linalg.norm(ref.x, axis=1)
@@ -180,7 +191,8 @@ def main():
             # the oracle's own sensitivity: y scaled by (1 + 2^-52 N(0,1)), a 1-ulp input change
             rng = np.random.default_rng(7)
             yp = c.y * (1.0 + 2.0 ** -52 * rng.standard_normal(c.y.shape))
-            refp = oc.solve_cube(algo, c.basis, yp, c.masks, ocfg, jobs=args.jobs, pool=pool, chunk=256)
+            refp = oc.solve_cube(algo, c.basis, yp, c.masks, ocfg, jobs=args.jobs, pool=pool,
+                                 chunk=256 if c.n_pixels < 200000 else 2048)
             sse_p, _ = psnr_parts(c.spectra, c.basis, refp.x)
             p_p = db(sse_p.sum(), peak, cnt)
             line.update({"psnr_oracle_1ulp_db": p_p, "dpsnr_oracle_1ulp_db": p_p - p_r,
