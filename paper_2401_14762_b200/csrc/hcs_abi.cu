@@ -60,6 +60,7 @@ size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
     b += 2 * align256(sizeof(double) * (size_t)Np * Np);   // fragS, fragT
     b += align256(sizeof(double) * (size_t)Np);            // u0
     if (algo == HCS_FISTA && P > 0) b += align256(sizeof(double) * (size_t)P);   // Lipschitz constants
+    if (algo == HCS_ADMM && P > 0) b += align256(sizeof(long long) * (size_t)P);  // uncertified-pixel list
   } else if (greedy(algo)) {
     // per-CTA global scratch for systems beyond the shared-memory region
     b += align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm);
@@ -138,6 +139,16 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
       if (e != cudaSuccess) return cuda_fail(e, "lipschitz_prepass_kernel");
     }
     hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, lip, x_out, st, pr, counter, err};
+    if (algo == HCS_ADMM) {
+      // pixels whose shrinkage is certified zero are solved by the O(N) pass;
+      // the slot engine takes the rest from the list (admm_zero_kernel)
+      long long* plist = reinterpret_cast<long long*>(lip);   // same offset as fista's Lipschitz array
+      unsigned long long* plist_n = reinterpret_cast<unsigned long long*>(ws + 16);
+      e = hcs::launch_admm_zero(args, plist, plist_n, sms, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "admm_zero_kernel");
+      args.plist = plist;
+      args.plist_n = plist_n;
+    }
     // persistent: one CTA (32 slots) or two CTAs (16 slots each) per SM
     const long long tiles = (P + slots - 1) / slots;
     const long long ctas = slots == 32 ? sms : 2LL * sms;

@@ -49,6 +49,7 @@ struct SlotState {
   int status[SL], iter[SL], flag[SL], rfail[SL], retired[SL], moff[SL], need_pf[SL];
   int nact[2];
   int exhausted;
+  long long np;           // pixels in the queue (P, or *plist_n)
 };
 
 // Slot-column layout of the GEMM input buffers: 32 slots (one CTA per SM) or 16
@@ -71,8 +72,13 @@ __device__ void prefetch_slot(const ConvexArgs& a, SlotState<SL>& ss, double* sy
   const int M = a.M, Mm = stage_mask_bytes(M);
   long long pid = 0;
   if (lane == 0) {
-    pid = ss.exhausted ? a.P : (long long)atomicAdd(a.counter, 1ull);
-    if (pid >= a.P) ss.exhausted = 1;
+    const long long q = ss.exhausted ? ss.np : (long long)atomicAdd(a.counter, 1ull);
+    if (q >= ss.np) {
+      ss.exhausted = 1;
+      pid = a.P;                       // none
+    } else {
+      pid = a.plist ? a.plist[q] : q;
+    }
     ss.npid[s] = pid;
   }
   pid = __shfl_sync(0xffffffffu, pid, 0);
@@ -275,6 +281,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   if (threadIdx.x == 0) {
     ss.exhausted = 0;
     ss.nact[0] = ss.nact[1] = 0;
+    ss.np = a.plist ? (long long)*a.plist_n : a.P;
   }
   __syncthreads();
   for (int s = w; s < SL; s += W) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
@@ -583,6 +590,135 @@ cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, co
 cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
                               int slots, cudaStream_t stream) {
   prep_basis_kernel<<<64, 256, 0, stream>>>(basis, N, Np, fragS, fragT, u0, slots == 32 ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// ADMM while the shrinkage provably zeroes every coefficient (solvers.py:206-245
+// with z = soft(x + w, lambda/alpha) = 0): with z = 0 the iteration is
+// diagonal in the sample domain.  For orthonormal Psi and W = Psi w,
+//     Psi x = u' = (yhat - alpha W) / (d + alpha),   w <- w + x  =>  W <- W + u',
+// the residual y - A x = yhat - u' on the measured rows, ||x - z|| = ||u'||,
+// and z = 0 is certified every pass by |x_i + w_i| <= ||x + w|| = ||u' + W||
+// <= (1 - 1e-9) lambda/alpha (Parseval; the margin covers the rounding of the
+// elementwise recurrence against the coefficient-domain one).  The same
+// iterates, iteration count and stop decisions as the slot engine, at
+// O(N) instead of 4 N^2 FLOP per iteration; a pixel whose certificate fails
+// (or whose measurements are not finite) is appended to plist and solved from
+// scratch by the slot engine.  One warp per pixel, rows n = lane + 32 k.
+__global__ void __launch_bounds__(256) admm_zero_kernel(ConvexArgs a, long long* plist,
+                                                        unsigned long long* plist_n) {
+  __shared__ double syw[8][kMaxN];
+  __shared__ uint8_t smw[8][kMaxN];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int N = a.N, M = a.M;
+  const double alpha = a.prm.alpha;
+  const double inv0 = 1.0 / alpha, inv1 = 1.0 / (1.0 + alpha);
+  const double bound = (a.prm.lam / alpha) * (1.0 - 1e-9);
+  const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+  constexpr int R = kMaxN / 32;
+  for (long long p = gw; p < a.P; p += nw) {
+    for (int n = lane; n < kMaxN; n += 32) {
+      syw[wl][n] = 0.0;
+      smw[wl][n] = 0;
+    }
+    __syncwarp();
+    bool nz = false, bad = false;
+    for (int j = lane; j < M; j += 32) {
+      const double v = a.y[p * M + j];
+      const int row = a.mask[p * M + j];
+      syw[wl][row] = v;
+      smw[wl][row] = 1;
+      nz |= (v != 0.0);
+      bad |= !isfinite(v);
+    }
+    nz = __any_sync(0xffffffffu, nz);
+    bad = __any_sync(0xffffffffu, bad);
+    __syncwarp();
+    const long long t0 = now_ns();
+    if (bad) {   // cho_solve raises (solvers.py:227); the engine flags it
+      if (lane == 0) plist[atomicAdd(plist_n, 1ull)] = p;
+      continue;
+    }
+    double* xo = a.x_out + p * N;
+    if (!nz) {   // y == 0: x = 0, 0 iterations, converged, delta 0, no admm_gap
+      for (int n = lane; n < N; n += 32) xo[n] = 0.0;
+      if (lane == 0) {
+        a.st.iterations[p] = 0;
+        a.st.converged[p] = 1;
+        a.st.final_delta[p] = 0.0;
+        a.st.failed_at[p] = -1;
+        if (a.st.admm_gap) a.st.admm_gap[p] = NaN;
+        if (a.st.lipschitz) a.st.lipschitz[p] = NaN;
+        if (a.st.elapsed) a.st.elapsed[p] = 0.0;
+        if (a.st.work) a.st.work[p] = 0.0;
+      }
+      continue;
+    }
+    int dec = stop_decision(1.0, 0, t0, a.prm);
+    double yh[R], inv[R], W[R], rp[R];
+    bool ms[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int n = lane + 32 * k;
+      yh[k] = syw[wl][n];
+      ms[k] = smw[wl][n] != 0;
+      inv[k] = ms[k] ? inv1 : inv0;
+      W[k] = 0.0;
+      rp[k] = yh[k];                   // r_0 = y on the measured rows
+    }
+    int it = 0;
+    double delta = 1.0, gap2 = 0.0;
+    bool certified = true, failed = false;
+    while (dec == kContinue) {
+      double dd = 0.0, s2 = 0.0, g2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (lane + 32 * k >= N) break;
+        const double up = (yh[k] + alpha * (-W[k])) * inv[k];
+        if (ms[k]) {
+          const double rn = yh[k] - up;
+          const double d = rn - rp[k];
+          dd += d * d;
+          rp[k] = rn;
+        }
+        const double xw = up + W[k];
+        s2 += xw * xw;
+        g2 += up * up;
+        W[k] += up;
+      }
+      dd = warp_sum(dd);
+      s2 = warp_sum(s2);
+      g2 = warp_sum(g2);
+      if (!(sqrt(s2) <= bound)) { certified = false; break; }
+      ++it;
+      delta = sqrt(dd);
+      gap2 = g2;
+      if (!isfinite(delta)) { failed = true; break; }
+      dec = stop_decision(delta, it, t0, a.prm);
+    }
+    if (!certified) {
+      if (lane == 0) plist[atomicAdd(plist_n, 1ull)] = p;
+      continue;
+    }
+    for (int n = lane; n < N; n += 32) xo[n] = 0.0;   // z = 0
+    if (lane == 0) {
+      a.st.iterations[p] = failed ? 0 : it;
+      a.st.converged[p] = (!failed && dec == kConverged) ? 1 : 0;
+      a.st.final_delta[p] = failed ? NaN : delta;
+      a.st.failed_at[p] = failed ? it : -1;
+      if (a.st.admm_gap) a.st.admm_gap[p] = failed ? NaN : (it == 0 ? 0.0 : sqrt(gap2));
+      if (a.st.lipschitz) a.st.lipschitz[p] = NaN;
+      if (a.st.elapsed) a.st.elapsed[p] = 1e-9 * (double)(now_ns() - t0);
+      if (a.st.work) a.st.work[p] = 12.0 * (double)N * (double)it;   // the elementwise pass, not 4 N^2
+    }
+  }
+}
+
+cudaError_t launch_admm_zero(const ConvexArgs& args, long long* plist, unsigned long long* plist_n, int sms,
+                             cudaStream_t stream) {
+  admm_zero_kernel<<<sms * 8, 256, 0, stream>>>(args, plist, plist_n);
   return cudaGetLastError();
 }
 

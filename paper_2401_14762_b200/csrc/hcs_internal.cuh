@@ -21,6 +21,10 @@ struct ConvexArgs {
   Params prm;
   unsigned long long* counter;
   int* err;
+  // optional pixel list (the ADMM pixels the zero-shrinkage pass could not
+  // certify): the engine works on plist[0 .. *plist_n) instead of 0 .. P-1
+  const long long* plist = nullptr;
+  const unsigned long long* plist_n = nullptr;
 };
 
 struct GreedyArgs {
@@ -40,6 +44,8 @@ struct GreedyArgs {
 // hcs_convex.cu
 cudaError_t launch_convex(int algo, const ConvexArgs& args, int slots, int grid, cudaStream_t stream);
 size_t convex_smem_bytes(int algo, int Np, int M, int slots);
+cudaError_t launch_admm_zero(const ConvexArgs& args, long long* plist, unsigned long long* plist_n, int sms,
+                             cudaStream_t stream);
 int convex_slots(int algo, int Np, int M);
 cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
                                      int sms, cudaStream_t stream);

@@ -334,3 +334,35 @@ def test_convex_slot_engines_agree(monkeypatch, algo, params):
     assert np.array_equal(it32, it16), f"{int((it32 != it16).sum())} iteration mismatches"
     assert np.max(np.abs(x32 - x16)) <= 1e-13 * max(np.max(np.abs(x32)), 1e-300), np.max(np.abs(x32 - x16))
     assert np.allclose(d32, d16, rtol=1e-12, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lam", [1.0, 3.0, 100.0])
+def test_admm_zero_shrinkage_pass_matches_oracle(lam):
+    """ADMM pixels whose shrinkage is certified zero are solved by the O(N)
+    sample-domain pass (admm_zero_kernel), the rest by the slot engine from the
+    pixel list; lambda = 1 and 3 mix both populations in one call.  Every pixel
+    must match the oracle: iterations, converged, x (1e-9), admm_gap (1e-9)."""
+    import torch
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    c = synth.generate(8, 50, 224, seed=33)
+    dev = torch.device("cuda")
+    cfg = SolverConfig(lam=lam, alpha=1.8, time_limit=None, max_iter=5000)
+    b = solve_batch("admm", torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev),
+                    torch.as_tensor(c.basis, device=dev), cfg)
+    torch.cuda.synchronize()
+    ref = oc.solve_cube("admm", c.basis, c.y, c.masks, oc.OracleConfig(lam=lam, alpha=1.8, max_iter=5000))
+    assert np.array_equal(b.iterations.cpu().numpy(), ref.iterations)
+    assert np.array_equal(b.converged.cpu().numpy().astype(bool), ref.converged)
+    x = b.x.cpu().numpy()
+    nr = np.linalg.norm(ref.x, axis=1)
+    err = np.linalg.norm(x - ref.x, axis=1)
+    assert np.all(np.where(nr > 0, err <= 1e-9 * nr, err <= 1e-12))
+    # admm_gap = ||x - z|| of the last pass: ~1e-9 at convergence, a difference
+    # of nearly equal iterates, so its rounding is absolute (~1e-15 ||x||)
+    gap = b.admm_gap.cpu().numpy()
+    assert np.all(np.abs(gap - ref.admm_gap) <= 1e-9 * ref.admm_gap + 1e-13 * np.maximum(nr, 1.0))
+    zero = np.linalg.norm(ref.x, axis=1) == 0
+    if lam == 100.0:
+        assert zero.all()
+    print(f"lambda {lam}: {int(zero.sum())} / {len(zero)} pixels with x = 0")
