@@ -139,6 +139,7 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
       if (e != cudaSuccess) return cuda_fail(e, "lipschitz_prepass_kernel");
     }
     hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, lip, x_out, st, pr, counter, err};
+    if (const char* ov = getenv("HCS_CONVEX_KSKIP")) args.kskip = atoi(ov) != 0;   // A/B experiments
     if (algo == HCS_ADMM) {
       // pixels whose shrinkage is certified zero are solved by the O(N) pass;
       // the slot engine takes the rest from the list (admm_zero_kernel)

@@ -50,6 +50,7 @@ struct SlotState {
   int nact[2];
   int exhausted;
   long long np;           // pixels in the queue (P, or *plist_n)
+  unsigned long long kmask;   // fista: k-steps of x_{k+1} with a nonzero in some slot
 };
 
 // Slot-column layout of the GEMM input buffers: 32 slots (one CTA per SM) or 16
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // SL * 256: row -> measurement index
   uint8_t* sm = pos + SL * kMaxN;                       // SL * stage_mask_bytes(M) staged mask rows
   const int cred = (SL == 32) ? col_of_reduced(lane) : col_of_reduced4(lane);
+  const bool use_kskip = (SL == 32) && ALGO == kFista && a.kskip;
 
   double p0[MAXRB][CB][2], p1[MAXRB][CB][2];
 #pragma unroll
@@ -360,7 +362,10 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       __syncwarp();
     }
-    if (threadIdx.x == 0) ss.nact[par ^ 1] = 0;
+    if (threadIdx.x == 0) {
+      ss.nact[par ^ 1] = 0;
+      ss.kmask = 0ull;
+    }
     __syncthreads();
     CMARK(0);
     for (int s = w; s < SL; s += W)
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     CMARK(1);
 
     double part[NV];
+    unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
     if (ALGO == kFista) {
       // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
       gemm(a.fragT, bufA);
@@ -416,14 +422,25 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             p0[rb][cb][i] = xn;
             bad |= !isfinite(xn);
             bufA[zi] = xn;
+            if (xn != 0.0) kbits |= 1ull << ((row0 + 8 * rb) >> 2);
           }
           if (bad) ss.flag[s] = 1;
         }
-      preload(mat2);   // next GEMM's first k-steps
+      if (use_kskip) {
+        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits);
+        const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits >> 32));
+        if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask, ((unsigned long long)hi << 32) | lo);
+      } else {
+        preload(mat2);   // next GEMM's first k-steps
+      }
       __syncthreads();
       CMARK(3);
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
-      gemm(a.fragS, bufA);
+      if (use_kskip) {
+        if constexpr (SL == 32) tile_gemm_masked(nrb, a.fragS, rb0, bufA, KS, ss.kmask, acc);
+      } else {
+        gemm(a.fragS, bufA);
+      }
       __syncthreads();
       CMARK(4);
 #pragma unroll

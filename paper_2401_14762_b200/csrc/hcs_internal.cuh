@@ -25,6 +25,7 @@ struct ConvexArgs {
   // certify): the engine works on plist[0 .. *plist_n) instead of 0 .. P-1
   const long long* plist = nullptr;
   const unsigned long long* plist_n = nullptr;
+  int kskip = 1;          // fista: skip the all-zero k-steps of Psi x_{k+1} (bitwise-identical)
 };
 
 struct GreedyArgs {

@@ -366,3 +366,25 @@ def test_admm_zero_shrinkage_pass_matches_oracle(lam):
     if lam == 100.0:
         assert zero.all()
     print(f"lambda {lam}: {int(zero.sum())} / {len(zero)} pixels with x = 0")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lam", [0.1, 0.01, 100.0])
+def test_fista_kstep_skip_bitwise(monkeypatch, lam):
+    """FISTA's second GEMM (Psi x_{k+1}) skips the k-steps whose four
+    coefficient rows are zero in every slot: the skipped products are exact
+    zeros, so results are bit-for-bit those of the dense GEMM."""
+    import torch
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    c = synth.generate(6, 50, 224, seed=44)
+    dev = torch.device("cuda")
+    args = (torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev), torch.as_tensor(c.basis, device=dev),
+            SolverConfig(lam=lam, time_limit=None, max_iter=5000))
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HCS_CONVEX_KSKIP", flag)
+        b = solve_batch("fista", *args)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.final_delta, b.converged)])
+    for u, v in zip(*outs):
+        assert np.array_equal(u, v)
