@@ -430,13 +430,14 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits);
         const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits >> 32));
         if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask, ((unsigned long long)hi << 32) | lo);
-      } else {
-        preload(mat2);   // next GEMM's first k-steps
       }
+      preload(mat2);   // next GEMM's first k-steps (the dense path's)
       __syncthreads();
       CMARK(3);
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
-      if (use_kskip) {
+      // the masked loop only when at most half the k-steps are active (it
+      // prefetches 2 steps ahead instead of 4: slower on a dense mask)
+      if (use_kskip && 2 * __popcll(ss.kmask) <= KS) {
         if constexpr (SL == 32) tile_gemm_masked(nrb, a.fragS, rb0, bufA, KS, ss.kmask, acc);
       } else {
         gemm(a.fragS, bufA);
