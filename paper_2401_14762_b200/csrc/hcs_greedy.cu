@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         double acc[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-#pragma unroll 2
+#pragma unroll 4
         for (int j = warp; j < M; j += 4) {
           const double rj = r[j];
           const double* row = a.basis + (size_t)msk[j] * N + lane;
