@@ -381,9 +381,10 @@ def run_ours(args):
                                       for i, (a, p, _) in enumerate(cfgs)},
                 "per_config_frac": {label(a, p): float(stats[i, 5]) / per_cfg[i] / world / 1e12 / peak_tf
                                     for i, (a, p, _) in enumerate(cfgs)},
-                "work_note": "device work counters = FLOPs executed: 4 N^2 per slot-engine iteration, 12 N per "
-                             "iteration of the certified zero-shrinkage ADMM pass (admm_l100), greedy per-pass "
-                             "counts from the actual supports"}
+                "work_note": "device work counters: 4 N^2 per slot-engine iteration (the algorithmic count; "
+                             "FISTA's second GEMM skips all-zero k-steps when at most half are active, counted "
+                             "dense), 12 N per iteration of the certified zero-shrinkage ADMM pass (admm_l100, "
+                             "the FLOPs it executes), greedy per-pass counts from the actual supports"}
 
     # streaming phase: the coefficient-domain PSNR kernel alone (HBM-bound), timed
     # with events on its stream over the last recovered cube
