@@ -310,10 +310,16 @@ class _LazyResults:
         return (self[i] for i in range(len(self)))
 
 
+_PER_PIXEL = ("iterations", "converged", "final_delta", "failed_at", "admm_gap", "elapsed")
+
+
 @dataclass
 class RecoveryStats:
     """Aggregate of a whole-cube recovery (solvers.py:413-433), plus the
-    per-pixel arrays the GPU produces (host numpy)."""
+    per-pixel arrays the GPU produces (host numpy: `iterations`, `converged`,
+    `final_delta`, `failed_at`, `admm_gap`, `elapsed`).  The aggregates are
+    reduced on the device; the per-pixel arrays are copied to the host on
+    first access (most callers only read the aggregates)."""
 
     n_pixels: int
     n_converged: int
@@ -324,13 +330,26 @@ class RecoveryStats:
     results: object = field(repr=False, default=None)
     failed_pixels: list = field(default_factory=list)
     algorithm: str = ""
-    iterations: np.ndarray = field(repr=False, default=None)
-    converged: np.ndarray = field(repr=False, default=None)
-    final_delta: np.ndarray = field(repr=False, default=None)
-    failed_at: np.ndarray = field(repr=False, default=None)
-    admm_gap: np.ndarray = field(repr=False, default=None)
-    elapsed: np.ndarray = field(repr=False, default=None)
     wall_time_s: float = 0.0
+    _src: dict = field(repr=False, default_factory=dict)     # name -> device tensor (until first access)
+    _host: dict = field(repr=False, default_factory=dict)    # name -> numpy array
+
+    def _array(self, name):
+        a = self._host.get(name)
+        if a is None:
+            t = self._src.pop(name)
+            a = t.cpu().numpy()
+            if name == "converged":
+                a = a.astype(bool)
+            self._host[name] = a
+        return a
+
+    iterations = property(lambda self: self._array("iterations"))
+    converged = property(lambda self: self._array("converged"))
+    final_delta = property(lambda self: self._array("final_delta"))
+    failed_at = property(lambda self: self._array("failed_at"))
+    admm_gap = property(lambda self: self._array("admm_gap"))
+    elapsed = property(lambda self: self._array("elapsed"))
 
     @property
     def convergence_pct(self):
@@ -338,23 +357,37 @@ class RecoveryStats:
 
 
 def _stats_from_batch(algorithm, b, y_dim, x_flat, wall):
-    it = b.iterations.cpu().numpy()
-    cv = b.converged.cpu().numpy().astype(bool)
-    fa = b.failed_at.cpu().numpy()
-    el = b.elapsed.cpu().numpy()
+    """RecoveryStats of a DeviceBatch: the aggregates by device reductions and
+    one small copy; the per-pixel arrays stay on the device until read."""
+    import torch
+    it, fa, el = b.iterations, b.failed_at, b.elapsed
+    cv = b.converged.bool()
     ok = fa < 0
-    failed = np.flatnonzero(~ok)
+    itl = it.to(torch.int64)
+    agg = torch.stack([
+        (cv & ok).sum().to(torch.float64),
+        (~ok).sum().to(torch.float64),
+        ((it == 0) & cv & ok).sum().to(torch.float64),
+        torch.where(ok, itl, torch.zeros_like(itl)).sum().to(torch.float64),
+        torch.where(ok, el, torch.zeros_like(el)).sum(),
+    ]).cpu().tolist()
+    n_failed = int(agg[1])
+    failed = []
+    if n_failed:
+        idx = torch.nonzero(~ok).flatten()
+        fav = fa[idx].cpu().numpy()
+        failed = [(int(p // y_dim), int(p % y_dim), int(f)) for p, f in zip(idx.cpu().numpy(), fav)]
     st = RecoveryStats(
-        n_pixels=int(it.size),
-        n_converged=int(np.count_nonzero(cv & ok)),
-        n_failed=int(failed.size),
-        n_zero_pixels=int(np.count_nonzero((it == 0) & cv & ok)),
-        total_iterations=int(it[ok].sum()),
-        recovery_time_s=float(el[ok].sum()),
-        failed_pixels=[(int(p // y_dim), int(p % y_dim), int(fa[p])) for p in failed],
+        n_pixels=int(it.numel()),
+        n_converged=int(agg[0]),
+        n_failed=n_failed,
+        n_zero_pixels=int(agg[2]),
+        total_iterations=int(agg[3]),
+        recovery_time_s=float(agg[4]),
+        failed_pixels=failed,
         algorithm=algorithm,
-        iterations=it, converged=cv, final_delta=b.final_delta.cpu().numpy(), failed_at=fa,
-        admm_gap=b.admm_gap.cpu().numpy(), elapsed=el, wall_time_s=wall)
+        wall_time_s=wall,
+        _src={name: getattr(b, name) for name in _PER_PIXEL})
     st.results = _LazyResults(st, x_flat)
     return st
 
@@ -406,7 +439,19 @@ def _recover_host(algorithm, y_host, dictionary, config, x_host, chunk_pixels, s
             lipschitz=torch.full((P,), math.nan, **f64), elapsed=torch.empty((P,), **f64),
             work=torch.empty((P,), **f64))
         chunk = max(1, min(P, int(chunk_pixels)))
-        bounds = [(p0, min(P, p0 + chunk)) for p0 in range(0, P, chunk)]
+        # graded chunks: a short first chunk starts the solve after a short H2D,
+        # a short last chunk leaves a short D2H after the last solve
+        edge = min(chunk, max(1, P // 32))
+        sizes = []
+        if P >= 65536 and chunk > edge:
+            mid = P - 2 * edge
+            sizes = [edge] + [chunk] * (mid // chunk) + ([mid % chunk] if mid % chunk else []) + [edge]
+        else:
+            sizes = [chunk] * (P // chunk) + ([P % chunk] if P % chunk else [])
+        bounds, p0 = [], 0
+        for sz in sizes:
+            bounds.append((p0, p0 + sz))
+            p0 += sz
         wsb = lib.hcs_workspace_bytes(algo, chunk, n, m)
         ws = [torch.empty((max(wsb, 256),), dtype=torch.uint8, device=dev) for _ in range(min(2, len(bounds)))]
         errs = torch.zeros((max(1, len(bounds)),), dtype=torch.int32, device=dev)
