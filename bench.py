@@ -434,7 +434,9 @@ def run_ours(args):
                 cube_h, st = recover_cube(y_h, dic, cfg, algo, out=outs[i % 2])
                 if k == 0:
                     h2d += y_h.numel() * 8 + masks_host.size
-                    d2h += cube_h.numel() * 8 + P * (4 + 1 + 8 + 4 + 8 + 8 + 8)
+                    # the cube, plus the five aggregate statistics reduced on the device
+                    # (per-pixel stats arrays are copied only when read)
+                    d2h += cube_h.numel() * 8 + 5 * 8
         torch.cuda.synchronize()
         te = time.perf_counter() - te
         tte = torch.tensor([te], dtype=torch.float64, device=dev)
