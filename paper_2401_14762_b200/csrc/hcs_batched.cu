@@ -63,7 +63,7 @@ cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t*
 // rank, 1 for the minimum-norm fallback).
 struct LsShared {
   double red[16];
-  int ipiv, flag;
+  int ipiv, flag, ctr;   // ctr must follow flag: ls_csne's Gram tile counter (flag[1])
 };
 
 __host__ __device__ inline size_t ls_batched_doubles(int M, int K) {
@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, cons
     int pth = 0;
     bool done = false;
     if (M >= K) {
+      if (threadIdx.x == 0) sh->ctr = 1;
       for (int idx = threadIdx.x; idx < ldb * nc; idx += blockDim.x) {
         const int c = idx / ldb, rr = idx - c * ldb;
         double v = 0.0;

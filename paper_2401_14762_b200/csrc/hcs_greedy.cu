@@ -49,6 +49,7 @@ struct GreedyShared {
   int count;
   int brk;
   int flag;
+  int ctr;   // must follow flag: ls_csne's Gram tile counter (flag[1])
 };
 
 // Shared-memory layout (doubles unless noted), identical on host and device.
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   };
 
   for (;;) {
-    if (tid == 0) g.pid = (long long)atomicAdd(a.counter, 1ull);
+    if (tid == 0) { g.pid = (long long)atomicAdd(a.counter, 1ull); g.ctr = 1; }
     __syncthreads();
     const long long pid = g.pid;
     if (pid >= a.P) break;

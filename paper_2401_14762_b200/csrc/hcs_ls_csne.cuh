@@ -71,7 +71,7 @@ struct CsneScratch {   // shared memory
   double* c;      // >= round8(K + 1): right-hand side / solution workspace
   double* r;      // >= M: residual
   double* red;    // >= 2 * warps
-  int* flag;      // 1
+  int* flag;      // 2: [0] guard flag, [1] Gram tile counter (1 between calls)
 };
 
 // Back substitution L^T x = c on the first K entries (c in/out, x overwrites c).  Warp 0.
@@ -239,8 +239,12 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
   double* G = sc.G;
   if (tid == 0) sc.flag[0] = 1;
   // ---- 1. augmented Gram, lower tiles, by DMMA ----------------------------------
+  // Warp 0 computes tile (0, 0) and factorises it at once (the first step of
+  // 2.) while the other warps take the remaining tiles from a shared counter
+  // (flag[1], 1 on entry); warp 0 joins them when its factorisation is done.
+  // Every tile is computed by the same instructions whichever warp takes it.
   const int ntiles = nbA * (nbA + 1) / 2;
-  for (int t = warp; t < ntiles; t += W) {
+  auto gram_tile = [&](int t) {
     const int bi = tri_row(t);
     const int bj = t - bi * (bi + 1) / 2;
     const double* ca = B + (8 * bi + (lane >> 2)) * ld + (lane & 3);
@@ -255,15 +259,26 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
     const int base = gtile(bi, bj) + (lane >> 2);
     G[base + (2 * (lane & 3)) * 8] = d0[0] + d1[0];
     G[base + (2 * (lane & 3) + 1) * 8] = d0[1] + d1[1];
+  };
+  if (warp == 0) {
+    gram_tile(0);
+    __syncwarp();
+    csne_diag_factor(G, sc, K, 0);
+  }
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&sc.flag[1], 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= ntiles) break;
+    gram_tile(t);
   }
   __syncthreads();
+  if (tid == 0) sc.flag[1] = 1;   // every warp is past the counter loop
   HCS_MARKP(ph, 4);
   // ---- 2. blocked right-looking Cholesky with look-ahead --------------------------
   // step kb: panel L_ik = G_ik L_kk^-T (all warps), then warp 0 updates the next
   // diagonal tile and factorises it while warps 1.. apply the rest of the
-  // trailing update G_ij -= L_ik L_jk^T.
-  if (warp == 0) csne_diag_factor(G, sc, K, 0);
-  __syncthreads();
+  // trailing update G_ij -= L_ik L_jk^T.  (The factorisation of tile 0 ran in 1.)
   HCS_MARKP(ph, 11);
   for (int kb = 0; kb < nb; ++kb) {
     const int o = 8 * kb;

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--cap", type=int, default=2000)
     ap.add_argument("--pixels", type=int, default=8000)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--dump", default=None, help="save x / iterations / flags of the last rep (.npz)")
     args = ap.parse_args()
     n = synth.CUBES[args.cube]["n"]
     rows = max(1, args.pixels // 100)
@@ -64,6 +65,9 @@ def main():
             nit = max(int(it.sum()), 1)
             print(f"  CTA cycles per pixel-iteration: {tot / nit:.0f} = " + ", ".join(
                 f"{nm} {ph[i] / nit:.0f}" for i, nm in enumerate(names)))
+    if args.dump:
+        np.savez(args.dump, x=out.x.cpu().numpy(), iterations=out.iterations.cpu().numpy(),
+                 converged=out.converged.cpu().numpy(), failed_at=out.failed_at.cpu().numpy())
 
 
 if __name__ == "__main__":
