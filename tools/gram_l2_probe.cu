@@ -1,7 +1,7 @@
 // Probe for the warp-per-pixel greedy plan: one warp forms the
 // lower 8 x 8 tiles of the Gram B^T B of B = basis[mask, S] (M rows, K columns)
 // by DMMA with its A/B fragments loaded straight from the L2-resident basis
-// (no shared-memory copy of B), pipelined over k-steps.  Reports cycles per
+// (no shared-memory copy of B), with 2, 4 or 8 k-steps of fragments in flight.  Reports cycles per
 // Gram per warp and Grams per second for several warps-per-SM counts, and
 // checks the tiles against a CPU Gram.
 //
@@ -25,6 +25,7 @@ constexpr int kMaxNB = 6;          // column blocks (K <= 48)
 constexpr int kTiles = kMaxNB * (kMaxNB + 1) / 2;
 
 // mask: P x M row indices; cols: P x K column indices; G out: P x kTiles x 64
+template <int D>
 __global__ void gram_l2_kernel(const double* __restrict__ basis, int N, int M, int K, int P,
                                const uint8_t* __restrict__ mask, const uint8_t* __restrict__ cols,
                                double* __restrict__ gout, long long* __restrict__ cyc, int reps) {
@@ -48,30 +49,33 @@ __global__ void gram_l2_kernel(const double* __restrict__ basis, int N, int M, i
     double acc[kTiles][2];
 #pragma unroll
     for (int t = 0; t < kTiles; ++t) acc[t][0] = acc[t][1] = 0.0;
-    // fragments of k-step ks for every block: f[b] = B[4 ks + (lane & 3)][8 b + (lane >> 2)]
-    double f0[kMaxNB], f1[kMaxNB];
-    auto load = [&](int ks, double (&f)[kMaxNB]) {
+    // fragments of k-step ks for every block: f[b] = B[4 ks + (lane & 3)][8 b + (lane >> 2)],
+    // D k-steps in flight
+    double f[D][kMaxNB];
+    auto load = [&](int ks, double (&fr)[kMaxNB]) {
       const int r = 4 * ks + (lane & 3);
       const int row = r < M ? mk[r] : -1;
 #pragma unroll
       for (int b = 0; b < kMaxNB; ++b)
-        f[b] = (b < nb && row >= 0 && col[b] >= 0) ? __ldg(basis + (size_t)row * N + col[b]) : 0.0;
+        fr[b] = (b < nb && row >= 0 && col[b] >= 0) ? __ldg(basis + (size_t)row * N + col[b]) : 0.0;
     };
-    auto mma = [&](const double (&f)[kMaxNB]) {
+    auto mma = [&](const double (&fr)[kMaxNB]) {
       int t = 0;
 #pragma unroll
       for (int bi = 0; bi < kMaxNB; ++bi)
 #pragma unroll
         for (int bj = 0; bj <= bi; ++bj, ++t)
-          if (bi < nb) dmma(acc[t], f[bi], f[bj]);
+          if (bi < nb) dmma(acc[t], fr[bi], fr[bj]);
     };
     const int KS = M4 >> 2;
-    load(0, f0);
-    for (int ks = 0; ks < KS; ks += 2) {
-      load(ks + 1, f1);
-      mma(f0);
-      load(ks + 2, f0);
-      if (ks + 1 < KS) mma(f1);
+#pragma unroll
+    for (int d = 0; d < D; ++d) load(d, f[d]);
+    for (int ks = 0; ks < KS; ks += D) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        if (ks + d < KS) mma(f[d]);
+        load(ks + d + D, f[d]);
+      }
     }
     int t = 0;
 #pragma unroll
@@ -104,7 +108,8 @@ int main(int argc, char** argv) {
   long long* d_cyc;
   cudaMalloc(&d_basis, basis.size() * 8);
   cudaMemcpy(d_basis, basis.data(), basis.size() * 8, cudaMemcpyHostToDevice);
-  for (int wps : {4, 8, 12, 16}) {
+  for (int depth : {2, 4, 8})
+  for (int wps : {8, 12, 16}) {
     const int cta_warps = 4, ctas = sms * (wps / cta_warps), P = ctas * cta_warps;
     std::vector<uint8_t> mask((size_t)P * M), cols((size_t)P * K);
     std::vector<int> idx(N);
@@ -124,13 +129,20 @@ int main(int argc, char** argv) {
     cudaMemcpy(d_mask, mask.data(), mask.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(d_cols, cols.data(), cols.size(), cudaMemcpyHostToDevice);
     const size_t smem = (size_t)cta_warps * kTiles * 64 * 8;
-    cudaFuncSetAttribute(gram_l2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gram_l2_kernel<<<ctas, 32 * cta_warps, smem>>>(d_basis, N, M, K, P, d_mask, d_cols, d_g, d_cyc, reps);
+    auto launch = [&]() {
+      if (depth == 2) gram_l2_kernel<2><<<ctas, 32 * cta_warps, smem>>>(d_basis, N, M, K, P, d_mask, d_cols, d_g, d_cyc, reps);
+      else if (depth == 4) gram_l2_kernel<4><<<ctas, 32 * cta_warps, smem>>>(d_basis, N, M, K, P, d_mask, d_cols, d_g, d_cyc, reps);
+      else gram_l2_kernel<8><<<ctas, 32 * cta_warps, smem>>>(d_basis, N, M, K, P, d_mask, d_cols, d_g, d_cyc, reps);
+    };
+    cudaFuncSetAttribute(gram_l2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gram_l2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gram_l2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    gram_l2_kernel<<<ctas, 32 * cta_warps, smem>>>(d_basis, N, M, K, P, d_mask, d_cols, d_g, d_cyc, reps);
+    launch();
     cudaEventRecord(e1);
     cudaError_t err = cudaDeviceSynchronize();
     if (err != cudaSuccess) { fprintf(stderr, "%s\n", cudaGetErrorString(err)); return 1; }
@@ -161,7 +173,7 @@ int main(int argc, char** argv) {
     double mean = 0.0;
     for (auto c : cyc) mean += (double)c;
     mean /= P;
-    printf("warps/SM %2d: %6.0f cycles per Gram per warp (M=%d K=%d), %.3g Grams/s, max |err| %.1e\n", wps, mean, M, K,
+    printf("depth %d warps/SM %2d: %6.0f cycles per Gram per warp (M=%d K=%d), %.3g Grams/s, max |err| %.1e\n", depth, wps, mean, M, K,
            (double)P * reps / (ms * 1e-3), maxerr);
     cudaFree(d_mask);
     cudaFree(d_cols);
