@@ -64,6 +64,7 @@ size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
   } else if (greedy(algo)) {
     // per-CTA global scratch for systems beyond the shared-memory region
     b += align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm);
+    b += align256(sizeof(double) * (size_t)N * N);   // transposed basis for the column gathers
   }
   return b;
 }
@@ -170,7 +171,11 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   long long grid = (long long)sms * per_sm;
   if (grid > P) grid = P;
   double* gscratch = reinterpret_cast<double*>(ws + kHeader);
-  hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch};
+  double* basis_t = reinterpret_cast<double*>(
+      ws + kHeader + align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm));
+  e = hcs::launch_transpose_basis(basis, N, basis_t, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "transpose_basis_kernel");
+  hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch, basis_t};
   e = hcs::launch_greedy(algo, args, (int)grid, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "greedy_kernel");
   return HCS_OK;

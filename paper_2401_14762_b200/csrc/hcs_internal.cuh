@@ -40,6 +40,7 @@ struct GreedyArgs {
   unsigned long long* counter;
   int* err;
   double* gscratch;      // per-CTA global LS scratch (systems beyond the shared-memory size)
+  const double* basis_t;   // Psi transposed (basis_t[c N + r] = Psi[r][c]): column gathers read one column
 };
 
 // hcs_convex.cu
@@ -57,6 +58,7 @@ cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t sme
 size_t greedy_smem_bytes(int M, int kalloc);
 int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap);
 size_t greedy_ls_doubles(int M);
+cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, cudaStream_t stream);
 int greedy_blocks_per_sm(int algo, int M, size_t smem);
 // hcs_batched.cu
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s,
