@@ -427,8 +427,8 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
           r[j] = rn;
         }
       } else {
-        // A x over the kx support columns from the dictionary rows in L2: lanes
-        // own rows, warps split the columns
+        // A x over the kx support columns from the transposed dictionary in L2:
+        // lanes own rows, warps split the columns
         double* pbuf = S;          // free again after solve()
         double ax[8];
 #pragma unroll
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int j = lane + 32 * q;
-            if (j < M) ax[q] += __ldg(a.basis + (size_t)msk[j] * N + col) * sc_;
+            if (j < M) ax[q] += __ldg(a.basis_t + (size_t)col * N + msk[j]) * sc_;
           }
         }
 #pragma unroll
