@@ -215,7 +215,7 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
     nat.check(lib.hcs_recover(algo, P, n, m, nat.ptr(basis), nat.ptr(y), nat.ptr(masks), prm, nat.ptr(out.x),
                               st, nat.ptr(workspace), workspace.numel(), sh))
     out.workspace = workspace
-    out.launches = (3 if algorithm in CONVEX_SOLVERS else 1) if P > 0 else 0   # prep + (lipschitz | zero pass) + engine
+    out.launches = (3 if algorithm in CONVEX_SOLVERS else 2) if P > 0 else 0   # convex: prep + (lipschitz | zero pass) + engine; greedy: basis transpose + engine
     if check_status:
         out.check_status(stream)
     return out
@@ -499,7 +499,7 @@ def _recover_host(algorithm, y_host, dictionary, config, x_host, chunk_pixels, s
     if bounds and int(errs.max().item()):   # the flag hcs_recover_status reads, per chunk
         raise ValueError("array must not contain infs or NaNs")
     full.workspace = ws[0] if ws else None
-    full.launches = sum((3 if algorithm in CONVEX_SOLVERS else 1) for _ in bounds)
+    full.launches = sum((3 if algorithm in CONVEX_SOLVERS else 2) for _ in bounds)
     return full
 
 
