@@ -71,42 +71,80 @@ def host_cores():
 
 # ------------------------------------------------------------------ CPU oracle leg
 
+CPU_STRIDE = 97
 
-def _oracle_rate(cube, solvers, budget_s, cores, seed=0, pool=None):
-    """Time the oracle on a bounded sample per solver config (one persistent
-    process pool over `cores` workers, OpenBLAS single-threaded per worker, as
-    BASELINE.md §2 prescribes).  Returns (spectra/s aggregated like the GPU
-    value, per-config rates, sample sizes)."""
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    from concurrent.futures import ProcessPoolExecutor
-    from oracle import cpu_solvers as oc
-    own = pool is None
-    if own:
-        pool = ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas)
-        list(pool.map(abs, range(4 * cores)))        # start the workers outside the timing
-    rng = np.random.default_rng(seed)
-    rates, sizes = {}, {}
-    P = cube.n_pixels
-    try:
-        for algo, params, cap in solvers:
-            cfg = oc.OracleConfig(max_iter=cap or 0, **params)
-            n = min(P, 4 * cores)
-            while True:
-                idx = np.sort(rng.choice(P, size=n, replace=False))
-                t0 = time.perf_counter()
-                oc.solve_cube(algo, cube.basis, cube.y[idx], cube.masks[idx], cfg,
-                              chunk=max(1, n // (4 * cores)), pool=pool)
-                dt = time.perf_counter() - t0
-                if dt >= 0.5 * budget_s or n >= P:
-                    break
-                n = int(min(P, max(2 * n, n * budget_s / max(dt, 1e-3))))
-            rates[label(algo, params)] = n / dt
-            sizes[label(algo, params)] = int(n)
-    finally:
-        if own:
-            pool.shutdown()
-    agg = len(solvers) / sum(1.0 / r for r in rates.values())
-    return agg, rates, sizes
+
+class CpuBaseline:
+    """The reference's algorithm on the host cores (the oracle port, one
+    worker process per core, OpenBLAS single-threaded per worker, as
+    SURVEY.md §8(d) / BASELINE.md §2 prescribe), timed on a fixed
+    deterministic sample of the workload cube: every 97th pixel by global
+    x-major index (18,327 of the scaling cube's 1,777,664, spread over all 16
+    tiles).  Each step solves, for every solver configuration, the next
+    round-robin chunk of that sample sized to ~``budget`` seconds of work;
+    a configuration's rate is chunk pixels / wall time of its pool map, the
+    step's value their harmonic aggregate (10 configs x P / sum of times, the
+    way `value` aggregates).  Also reports the sum of per-pixel solve times
+    (the reference's recovery_time_s semantics, solvers.py:510)."""
+
+    def __init__(self, workload, budget, cores, stride=CPU_STRIDE):
+        os.environ["OPENBLAS_NUM_THREADS"] = "1"
+        from concurrent.futures import ProcessPoolExecutor
+        from oracle import cpu_solvers as oc
+        self.oc = oc
+        cube_name, self.solvers = WORKLOADS[workload]
+        spec = synth.CUBES[cube_name]
+        self.shape = [spec["x_dim"], spec["y_dim"], spec["n"]]
+        self.sample = synth.generate_strided(cube_name, stride, workers=min(16, cores))
+        self.stride, self.budget, self.cores = stride, budget, cores
+        self.pool = ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas)
+        list(self.pool.map(abs, range(4 * cores)))        # start the workers outside the timing
+        self.offset = {label(a, p): 0 for a, p, _ in self.solvers}
+        self.size = {label(a, p): 4 * cores for a, p, _ in self.solvers}
+
+    def step(self):
+        S = self.sample.n_pixels
+        rates, sizes, sum_el = {}, {}, {}
+        for algo, params, cap in self.solvers:
+            lab = label(algo, params)
+            cfg = self.oc.OracleConfig(max_iter=cap or 0, **params)
+            n = min(self.size[lab], S)
+            idx = (self.offset[lab] + np.arange(n)) % S
+            y, masks = np.ascontiguousarray(self.sample.y[idx]), np.ascontiguousarray(self.sample.masks[idx])
+            t0 = time.perf_counter()
+            res = self.oc.solve_cube(algo, self.sample.basis, y, masks, cfg, chunk=max(1, n // (4 * self.cores)),
+                                     pool=self.pool)
+            dt = time.perf_counter() - t0
+            rates[lab], sizes[lab], sum_el[lab] = n / dt, n, float(res.elapsed.sum())
+            self.offset[lab] = (self.offset[lab] + n) % S
+            self.size[lab] = int(min(S, max(4 * self.cores, n * self.budget / max(dt, 1e-3))))
+        agg = len(rates) / sum(1.0 / r for r in rates.values())
+        return agg, rates, sizes, sum_el
+
+    def run(self, warmup, steps):
+        vals = []
+        for k in range(warmup + steps):
+            v = self.step()
+            if k >= warmup:
+                vals.append(v)
+        value = float(np.mean([v[0] for v in vals]))
+        labs = list(vals[0][1])
+        per = {k: float(np.mean([v[1][k] for v in vals])) for k in labs}
+        px = {k: int(sum(v[2][k] for v in vals)) for k in labs}
+        sel = {k: float(sum(v[3][k] for v in vals)) for k in labs}
+        return {
+            "value": value, "unit": "spectra/s", "cores": self.cores, "kind": "port",
+            "sample": (f"every {self.stride}th pixel of the {'x'.join(map(str, self.shape))} workload cube "
+                       f"(global x-major index p % {self.stride} == 0: {self.sample.n_pixels} px over all tiles); "
+                       f"per step and solver config the next round-robin chunk of ~{self.budget:g}s of work; "
+                       f"{steps} timed steps after {warmup} warm-up"),
+            "per_solver": per, "pixels_timed": px,
+            "sum_elapsed_s": sel,
+            "rate_from_sum_elapsed": {k: self.cores * px[k] / sel[k] for k in labs if sel[k] > 0},
+        }
+
+    def close(self):
+        self.pool.shutdown()
 
 
 def run_reference(args):
@@ -114,36 +152,25 @@ def run_reference(args):
     if rank != 0:
         return 0
     cube_name, solvers = WORKLOADS[args.workload]
-    spec = dict(synth.CUBES[cube_name])
-    # a bounded sample of the workload: the first tile (same generator, seed 0)
-    if "tiles" in spec:
-        tx, ty = spec.pop("tiles")
-        spec["x_dim"] //= tx
-        spec["y_dim"] //= ty
-    cube = synth.generate(seed=0, **spec)
+    spec = synth.CUBES[cube_name]
     cores = host_cores()
-    vals = []
-    from concurrent.futures import ProcessPoolExecutor
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    from oracle.cpu_solvers import single_thread_blas
-    with ProcessPoolExecutor(max_workers=cores, initializer=single_thread_blas) as pool:
-        list(pool.map(abs, range(4 * cores)))
-        for step in range(args.warmup + args.steps):
-            agg, rates, sizes = _oracle_rate(cube, solvers, args.ref_budget, cores, seed=step, pool=pool)
-            if step >= args.warmup:
-                vals.append((agg, rates, sizes))
-    value = float(np.mean([v[0] for v in vals]))
+    cb = CpuBaseline(args.workload, args.ref_budget, cores)
+    try:
+        res = cb.run(args.warmup, args.steps)
+    finally:
+        cb.close()
+    value = res["value"]
+    P = spec["x_dim"] * spec["y_dim"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "spectra/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generator hcs-synth-v1)",
-        "config": {"workload": args.workload, "cube": cube_name, "solvers": [label(a, p) for a, p, _ in solvers]},
-        "per_solver": {k: float(np.mean([v[1][k] for v in vals])) for k in vals[0][1]},
-        "cpu_baseline": {"value": value, "unit": "spectra/s", "cores": cores, "kind": "port",
-                         "sample": f"per step and solver config ~{args.ref_budget:g}s of oracle work on random "
-                                   f"pixels of tile 0 of the workload cube ({cube.n_pixels} px), "
-                                   f"sizes {vals[-1][2]}"},
+        "config": {"workload": args.workload, "cube": cube_name, "shape": [spec["x_dim"], spec["y_dim"], spec["n"]],
+                   "pixels": P, "measured_bands": synth.measured_count(spec["n"]),
+                   "solvers": [label(a, p) for a, p, _ in solvers], "sample": res["sample"]},
+        "per_solver": res["per_solver"],
+        "cpu_baseline": res,
         "e2e": {"value": value, "unit": "spectra/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -231,13 +258,12 @@ def run_ours(args):
     from paper_2401_14762_b200.solvers import SolverConfig, recover_cube, solve_batch
     from paper_2401_14762_b200.transform import Dictionary
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local = parallel.dist_env()
+    if world > torch.cuda.device_count():
+        raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    parallel.init_from_env("nccl", dev)
     _native.load()
 
     cube_name, solvers = WORKLOADS[args.workload]
@@ -290,35 +316,12 @@ def run_ours(args):
         del keys_d
     cfgs = [(a, p, SolverConfig(time_limit=None, max_iter=cap, **p)) for a, p, cap in solvers]
     nsolv = len(cfgs)
-    stats_d = torch.zeros((nsolv, len(parallel.STAT_FIELDS)), dtype=torch.float64, device=dev)
-    psnr_d = torch.zeros((nsolv, 2), dtype=torch.float64, device=dev)    # sse, max|ref| (this rank)
     # PSNR peak = max |reference spectra| over the whole cube: input-derived, reduced once at setup
     peak_ref = float(parallel.all_reduce_max(spectra_d.abs().max().reshape(1)).item())
+    # the timed step: every configuration on this rank's slab + PSNR partials + one all-reduce
+    step = parallel.ShardedStep([(a, c) for a, _, c in cfgs], y_d, masks_d, basis_d, coeffs_d)
+    stats_d = step.stats
     torch.cuda.synchronize()
-
-    out = None
-    launches_per_step = 0
-
-    def step(record=None):
-        nonlocal out, launches_per_step
-        launches = 0
-        psnr_d.zero_()
-        for i, (algo, params, cfg) in enumerate(cfgs):
-            if record is not None:
-                record[i][0].record()
-            b = solve_batch(algo, y_d, masks_d, basis_d, cfg, check_status=False, out=out)
-            if record is not None:
-                record[i][1].record()
-            out = b
-            # PSNR's squared error in the coefficient domain (Parseval):
-            # one HBM stream over the reference and recovered coefficients
-            sse_coeff_partials(coeffs_d, b.x, out=psnr_d[i, :1])
-            for f, v in enumerate(parallel.local_stats(b)):
-                stats_d[i, 1 + f] = v
-            launches += b.launches + 1
-        stats_d[:, 0] = psnr_d[:, 0]
-        parallel.all_reduce_stats(stats_d)   # the one data-path collective
-        launches_per_step = launches
 
     # FP64 tensor peak of this GPU (roofline denominator)
     peak_tf = _native.dmma_peak_tflops()
@@ -331,8 +334,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         print(f"[bench] warm-up step {time.perf_counter() - tw:.2f}s", file=sys.stderr, flush=True)
     torch.cuda.synchronize()
-    if out is not None:
-        out.check_status()
+    step.check_errors()
 
     ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in cfgs]
           for _ in range(args.steps)]
@@ -350,6 +352,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    step.check_errors()
+    out = step.out
     elapsed = t0.elapsed_time(t1) / 1e3
     per_cfg = np.array([[ev[k][i][0].elapsed_time(ev[k][i][1]) / 1e3 for i in range(nsolv)]
                         for k in range(args.steps)]).mean(axis=0)
@@ -451,14 +455,11 @@ def run_ours(args):
     # ---- CPU baseline (rank 0, N = 1 only) --------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        tile = synth.generate(spec["x_dim"] // spec.get("tiles", (1, 1))[0],
-                              spec["y_dim"] // spec.get("tiles", (1, 1))[1], n, seed=0)
-        cores = host_cores()
-        agg, rates, sizes = _oracle_rate(tile, solvers, args.cpu_budget, cores)
-        cpu = {"value": agg, "unit": "spectra/s", "cores": cores, "kind": "port",
-               "sample": f"~{args.cpu_budget:g}s of oracle work per solver config on random pixels of tile 0 "
-                         f"of the workload cube; sizes {sizes}",
-               "per_solver": rates}
+        cb = CpuBaseline(args.workload, args.ref_budget, host_cores())
+        try:
+            cpu = cb.run(1, 2)
+        finally:
+            cb.close()
 
     if rank == 0:
         line = {
@@ -471,7 +472,7 @@ def run_ours(args):
                        "pixels": P_total, "measured_bands": m, "solvers": [label(a, p) for a, p, _ in cfgs],
                        "parallelism": f"pixel-row slabs x{world}", "l2": "inputs (1.28 GB/step) > 126 MB L2; no flush"},
             "per_solver": per_solver, "quality": quality,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": step.launches * args.steps,
             "clocks": clk, "generation_s": t_gen, "input_side": input_side, "streaming": streaming,
         }
         print(json.dumps(line), flush=True)
@@ -488,8 +489,8 @@ def main():
     ap.add_argument("--workload", default="scaling", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=1)
-    ap.add_argument("--cpu-budget", type=float, default=2.0, help="seconds of oracle work per solver config")
-    ap.add_argument("--ref-budget", type=float, default=0.3)
+    ap.add_argument("--ref-budget", type=float, default=1.0,
+                    help="seconds of CPU work per solver config per step (reference arm and the cpu_baseline leg)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only", default="", help="comma-separated solver labels (diagnostics)")
@@ -498,6 +499,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command as N ranks (torch.distributed.run, 127.0.0.1)
+        from paper_2401_14762_b200 import parallel
+        return parallel.spawn_ranks(args.gpus, [str(Path(__file__).resolve()), *sys.argv[1:]])
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -19,7 +19,16 @@
  *   - `basis` is the N x N orthonormal synthesis matrix Psi (f = Psi c) and
  *     pixel p's dictionary is A_p = Psi[mask_p, :] (the reference's
  *     Dictionary.matrix, transform.py:267-281, with one mask per pixel);
- *   - N <= 256 (band indices are uint8), 1 <= M <= N, masks strictly increasing;
+ *   - N <= 256 (band indices are uint8), 1 <= M <= N;
+ *   - masks: each pixel's M band indices strictly increasing and < N.  The
+ *     library checks this on the device before any solver kernel reads a
+ *     mask: a violation makes every solver kernel of the call exit without
+ *     writing outputs and hcs_recover_status() return HCS_EINVAL;
+ *   - `basis` must be orthonormal (Psi^T Psi = I): the FISTA / ADMM closed
+ *     forms, the sample-domain Lipschitz constant and the coefficient-domain
+ *     PSNR rely on it.  A non-orthonormal basis is UNDEFINED BEHAVIOUR (silently
+ *     wrong results); hcs_check_basis() measures max |Psi^T Psi - I| once per
+ *     basis (the Python Dictionary rejects > 1e-10, transform.py:170-173);
  *   - all calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy
  *     default stream) and reentrant; no global mutable state;
  *   - return codes: HCS_OK, HCS_EINVAL (bad arguments: the Python layer raises
@@ -98,7 +107,14 @@ int hcs_abi_version(void);
 /* Human-readable message for the last error on this host thread. */
 const char* hcs_last_error(void);
 
-/* Device workspace hcs_recover needs for (algo, P, N, M). */
+/* Device workspace hcs_recover needs for (algo, P, N, M), sized for the
+ * device current at this call.  Layout (ABI 1.1; opaque to callers): a 256 B
+ * header (work-queue counters, the error word hcs_recover_status reads, the
+ * spill count of the warp-per-pixel gOMP kernel); FISTA / ADMM: the basis in
+ * DMMA fragment order (twice), a start vector, per-pixel Lipschitz constants
+ * or the ADMM pixel list; gOMP / BIHT / CoSaMP: the transposed basis, a
+ * P-entry spill list and per-CTA least-squares scratch (hcs_recover never
+ * launches more CTAs than the workspace holds scratch for). */
 size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M);
 
 /* Recover P pixels with one algorithm: the body of recover_cube
@@ -107,9 +123,18 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis,
                 const double* y, const uint8_t* mask, const hcs_params* prm, double* x_out,
                 const hcs_stats* stats, void* workspace, size_t workspace_bytes, void* stream);
 
-/* After the stream has executed a hcs_recover call on `workspace`: HCS_OK or
- * HCS_ENONFINITE (reads 4 bytes from the workspace; synchronises `stream`). */
+/* Number of kernels one hcs_recover call with these arguments launches. */
+int hcs_recover_launches(int algo, int32_t N, int32_t M, const hcs_params* prm);
+
+/* After the stream has executed a hcs_recover call on `workspace`: HCS_OK,
+ * HCS_EINVAL (a mask entry out of range or not strictly increasing; outputs
+ * not written) or HCS_ENONFINITE (non-finite measurements); reads 4 bytes
+ * from the workspace and synchronises `stream`. */
 int hcs_recover_status(const void* workspace, void* stream);
+
+/* max_ij |(Psi^T Psi - I)_ij| of the N x N basis (device pointer), written to
+ * *max_dev_out (host); synchronises `stream`. */
+int hcs_check_basis(int32_t N, const double* basis, double* max_dev_out, void* stream);
 
 /* Batched kernels of hypercs.kernels (kernels.py:14-76). */
 int hcs_soft_threshold(int64_t n, const double* v, double t, double* out, void* stream);

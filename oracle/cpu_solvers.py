@@ -39,6 +39,7 @@ classification of SURVEY.md §8(c): entries are
 
 import math
 import os
+import time
 from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass
 
@@ -198,6 +199,7 @@ class PixelResult:
     admm_gap: float = math.nan
     failed_at: int = -1          # iteration of a NumericalFailure, -1 if none
     lipschitz: float = math.nan
+    elapsed: float = 0.0         # seconds spent on the pixel (dictionary + solve)
 
 
 class _Failure(Exception):
@@ -418,6 +420,7 @@ class CubeResult:
     failed_at: np.ndarray    # (P,) int32, -1 ok
     lipschitz: np.ndarray    # (P,)
     traces: list | None = None
+    elapsed: np.ndarray | None = None   # (P,) seconds per pixel
 
 
 def single_thread_blas():
@@ -435,8 +438,11 @@ def _solve_range(args):
     out = []
     for p in range(y.shape[0]):
         trace = [] if want_trace else None
+        t0 = time.perf_counter()
         a = basis[masks[p].astype(np.intp), :]
-        out.append((solve_pixel(algo, y[p], a, cfg, trace), trace))
+        r = solve_pixel(algo, y[p], a, cfg, trace)
+        r.elapsed = time.perf_counter() - t0     # SolverResult.elapsed semantics (solvers.py:166, 201)
+        out.append((r, trace))
     return out
 
 
@@ -468,6 +474,7 @@ def solve_cube(algo, basis, y, masks, cfg, jobs=1, trace=False, chunk=64, pool=N
         failed_at=np.array([r.failed_at for r, _ in flat], dtype=np.int32),
         lipschitz=np.array([r.lipschitz for r, _ in flat]),
         traces=[t for _, t in flat] if trace else None,
+        elapsed=np.array([r.elapsed for r, _ in flat]),
     )
 
 

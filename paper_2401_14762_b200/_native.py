@@ -20,7 +20,7 @@ EXPORTS = (
     "hcs_abi_version", "hcs_last_error", "hcs_workspace_bytes", "hcs_recover", "hcs_recover_status",
     "hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta", "hcs_lipschitz",
     "hcs_psnr_partials", "hcs_dmma_peak_tflops", "hcs_synth_spectra", "hcs_sparsify_measure",
-    "hcs_sse_coeff_partials",
+    "hcs_sse_coeff_partials", "hcs_recover_launches", "hcs_check_basis",
 )
 
 
@@ -77,6 +77,10 @@ def load(path=None):
     lib.hcs_recover.restype = ctypes.c_int
     lib.hcs_recover.argtypes = [ctypes.c_int, i64, i32, i32, vp, vp, vp, ctypes.POINTER(HcsParams), vp,
                                 ctypes.POINTER(HcsStats), vp, ctypes.c_size_t, vp]
+    lib.hcs_check_basis.restype = ctypes.c_int
+    lib.hcs_check_basis.argtypes = [i32, vp, ctypes.POINTER(ctypes.c_double), vp]
+    lib.hcs_recover_launches.restype = ctypes.c_int
+    lib.hcs_recover_launches.argtypes = [ctypes.c_int, i32, i32, ctypes.POINTER(HcsParams)]
     lib.hcs_recover_status.restype = ctypes.c_int
     lib.hcs_recover_status.argtypes = [vp, vp]
     lib.hcs_soft_threshold.argtypes = [i64, vp, dbl, vp, vp]

@@ -45,14 +45,32 @@ def up_to_date():
 
 
 def build(force=False, verbose=False):
+    """Compile each translation unit in parallel (-c), then link the shared object."""
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", *sources()]
-    if verbose:
-        print(" ".join(cmd))
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+    nvcc = nvcc_path()
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory(prefix="hcs_build_") as tmp:
+        jobs = [(src, str(Path(tmp) / (Path(src).stem + ".o"))) for src in sources()]
+
+        def compile_one(job):
+            cmd = [nvcc, *flags, "-c", "-o", job[1], job[0]]
+            if verbose:
+                print(" ".join(cmd))
+            return subprocess.run(cmd, capture_output=True, text=True)
+
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+            results = list(ex.map(compile_one, jobs))
+        for res in results:
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB) + ".tmp",
+               *(o for _, o in jobs)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
     os.replace(str(LIB) + ".tmp", LIB)
     return LIB
 

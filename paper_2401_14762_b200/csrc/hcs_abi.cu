@@ -45,11 +45,29 @@ bool greedy(int algo) { return algo == HCS_GOMP || algo == HCS_BIHT || algo == H
 constexpr size_t kGreedySmemCap = 200 * 1024;
 constexpr int kMaxGreedyPerSm = 8;
 
+// Greedy workspace (ABI 1.1): [header 256 B: queue counter, error flag,
+// spill count, spill-queue counter][transposed basis N x N doubles][spill
+// list P x int64][per-CTA LS scratch, greedy_ls_doubles(M) doubles per CTA]
+struct GreedyWs {
+  size_t basis_t, spill, scratch;
+  long long slots;   // CTA scratch slots in a workspace of `bytes` bytes (0: not computed)
+};
+
+GreedyWs greedy_ws(int64_t P, int32_t N, int32_t M, size_t bytes) {
+  GreedyWs w;
+  w.basis_t = kHeader;
+  w.spill = w.basis_t + align256(sizeof(double) * (size_t)N * N);
+  w.scratch = w.spill + align256(sizeof(long long) * (size_t)(P > 0 ? P : 1));
+  const size_t per = sizeof(double) * hcs::greedy_ls_doubles(M);
+  w.slots = bytes > w.scratch ? (long long)((bytes - w.scratch) / per) : 0;
+  return w;
+}
+
 }  // namespace
 
 extern "C" {
 
-int hcs_abi_version(void) { return 100; }
+int hcs_abi_version(void) { return 101; }
 
 const char* hcs_last_error(void) { return g_err.c_str(); }
 
@@ -62,9 +80,9 @@ size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
     if (algo == HCS_FISTA && P > 0) b += align256(sizeof(double) * (size_t)P);   // Lipschitz constants
     if (algo == HCS_ADMM && P > 0) b += align256(sizeof(long long) * (size_t)P);  // uncertified-pixel list
   } else if (greedy(algo)) {
+    b = greedy_ws(P, N, M, 0).scratch;
     // per-CTA global scratch for systems beyond the shared-memory region
     b += align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm);
-    b += align256(sizeof(double) * (size_t)N * N);   // transposed basis for the column gathers
   }
   return b;
 }
@@ -120,13 +138,17 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(ws);
   int* err = reinterpret_cast<int*>(ws + 8);
   const int sms = num_sms();
+  // masks: strictly increasing band indices < N, checked on the device before
+  // any solver kernel reads one (HCS_EINVAL from hcs_recover_status)
+  e = hcs::launch_validate_masks(P, M, N, mask, err, sms, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "validate_masks_kernel");
 
   if (algo == HCS_FISTA || algo == HCS_ADMM) {
     const int Np = pad16(N);
     const int calgo = algo == HCS_FISTA ? hcs::kFista : hcs::kAdmm;
     const int slots = hcs::convex_slots(calgo, Np, M);
-    if (hcs::convex_smem_bytes(calgo, Np, M, slots) > (size_t)kSmemPerBlock)
-      return fail(HCS_EINVAL, "convex solvers: 32 pixel slots of N = " + std::to_string(N) + ", M = " +
+    if (slots == 0)
+      return fail(HCS_EINVAL, "convex solvers: 16 pixel slots of N = " + std::to_string(N) + ", M = " +
                                   std::to_string(M) + " exceed the 227 KB shared memory of one SM");
     double* fragS = reinterpret_cast<double*>(ws + kHeader);
     double* fragT = reinterpret_cast<double*>(ws + kHeader + align256(sizeof(double) * (size_t)Np * Np));
@@ -136,7 +158,7 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     e = hcs::launch_prep_basis(basis, N, Np, fragS, fragT, u0, slots, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_basis_kernel");
     if (algo == HCS_FISTA) {
-      e = hcs::launch_lipschitz_prepass(P, M, mask, u0, lip, sms, stream);
+      e = hcs::launch_lipschitz_prepass(P, M, mask, u0, lip, err, sms, stream);
       if (e != cudaSuccess) return cuda_fail(e, "lipschitz_prepass_kernel");
     }
     hcs::ConvexArgs args{(long long)P, N, Np, M, y, mask, fragT, fragS, u0, lip, x_out, st, pr, counter, err};
@@ -153,7 +175,7 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     }
     // persistent: one CTA (32 slots) or two CTAs (16 slots each) per SM
     const long long tiles = (P + slots - 1) / slots;
-    const long long ctas = slots == 32 ? sms : 2LL * sms;
+    const long long ctas = (long long)sms * hcs::convex_ctas_per_sm(calgo, Np, M, slots);
     const int grid = (int)(tiles < ctas ? tiles : ctas);
     e = hcs::launch_convex(calgo, args, slots, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "convex_kernel");
@@ -169,15 +191,67 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   if (per_sm < 1) per_sm = 1;
   if (per_sm > kMaxGreedyPerSm) per_sm = kMaxGreedyPerSm;
   long long grid = (long long)sms * per_sm;
-  if (grid > P) grid = P;
-  double* gscratch = reinterpret_cast<double*>(ws + kHeader);
-  double* basis_t = reinterpret_cast<double*>(
-      ws + kHeader + align256(sizeof(double) * hcs::greedy_ls_doubles(M) * (size_t)num_sms() * kMaxGreedyPerSm));
+  // the CTA scratch slots the workspace holds (sized by hcs_workspace_bytes on
+  // the device current at that call): never launch more CTAs than slots
+  const GreedyWs gw = greedy_ws(P, N, M, workspace_bytes);
+  if (grid > gw.slots) grid = gw.slots;
+  double* basis_t = reinterpret_cast<double*>(ws + gw.basis_t);
+  long long* spill_list = reinterpret_cast<long long*>(ws + gw.spill);
+  double* gscratch = reinterpret_cast<double*>(ws + gw.scratch);
   e = hcs::launch_transpose_basis(basis, N, basis_t, stream);
   if (e != cudaSuccess) return cuda_fail(e, "transpose_basis_kernel");
   hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch, basis_t};
+  // gOMP solves by Householder QR (the reference's algorithm): its
+  // iteration-2 selections are made on roundoff-level residuals, and CSNE's
+  // more accurate solutions shift which noise columns win (2.5x the oracle's
+  // 1-ulp tie rate and cube PSNR outside the oracle's 1-ulp band,
+  // tools/gomp_rounding_study.py, profiles/gomp_ls_statistics_r02.txt);
+  // BIHT / CoSaMP keep the CSNE fast path
+  args.ls_mode = algo == HCS_GOMP ? 1 : 0;
+  if (const char* ov = getenv("HCS_GREEDY_LS")) args.ls_mode = atoi(ov);   // A/B experiments
+  bool warp_path = algo == HCS_GOMP && args.ls_mode == 1 && hcs::gomp_warp_supported(N, M, prm->kappa);
+  if (const char* ov = getenv("HCS_GOMP_WARP")) warp_path = warp_path && atoi(ov) != 0;
+  if (warp_path) {
+    // warp-per-pixel Householder gOMP; the pixels it spills (supports beyond
+    // 33 columns, rank guard) are re-solved from scratch by the CTA kernel
+    unsigned long long* spill_n = reinterpret_cast<unsigned long long*>(ws + 16);
+    e = hcs::launch_gomp_warp(args, hcs::GwSpill{spill_n, spill_list}, sms, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gomp_warp_kernel");
+    args.counter = reinterpret_cast<unsigned long long*>(ws + 24);
+    args.plist = spill_list;
+    args.plist_n = spill_n;
+  }
   e = hcs::launch_greedy(algo, args, (int)grid, smem, stream);
   if (e != cudaSuccess) return cuda_fail(e, "greedy_kernel");
+  return HCS_OK;
+}
+
+int hcs_recover_launches(int algo, int32_t N, int32_t M, const hcs_params* prm) {
+  if (!prm || algo < HCS_FISTA || algo > HCS_COSAMP) return 0;
+  if (algo == HCS_FISTA || algo == HCS_ADMM) return 4;   // mask check + basis prep + (Lipschitz | zero pass) + slot engine
+  bool warp_path = algo == HCS_GOMP && hcs::gomp_warp_supported(N, M, prm->kappa);
+  if (const char* ov = getenv("HCS_GREEDY_LS")) warp_path = warp_path && atoi(ov) == 1;
+  if (const char* ov = getenv("HCS_GOMP_WARP")) warp_path = warp_path && atoi(ov) != 0;
+  return warp_path ? 4 : 3;   // mask check + basis transpose + (warp kernel +) CTA kernel
+}
+
+int hcs_check_basis(int32_t N, const double* basis, double* max_dev_out, void* stream_) {
+  if (N < 1 || N > HCS_MAX_N) return fail(HCS_EINVAL, "N must be in [1, 256]");
+  if (!basis || !max_dev_out) return fail(HCS_EINVAL, "null array");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "check_basis alloc");
+  unsigned long long h = 0;
+  e = cudaMemsetAsync(d, 0, sizeof(unsigned long long), stream);
+  if (e == cudaSuccess) e = hcs::launch_basis_gram_dev(N, basis, d, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, stream);
+  cudaFreeAsync(d, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "check_basis");
+  double dev;
+  memcpy(&dev, &h, sizeof(dev));
+  *max_dev_out = dev;
   return HCS_OK;
 }
 
@@ -188,6 +262,7 @@ int hcs_recover_status(const void* workspace, void* stream_) {
                                   cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return cuda_fail(e, "status");
+  if (flag & hcs::kErrMask) return fail(HCS_EINVAL, "mask entries must be strictly increasing band indices < N");
   if (flag) return fail(HCS_ENONFINITE, "array must not contain infs or NaNs");
   return HCS_OK;
 }

@@ -71,13 +71,16 @@ __host__ __device__ inline size_t ls_batched_doubles(int M, int K) {
   return blk > piv ? blk : piv;
 }
 
+// gscr: per-CTA global scratch for B and its Gram when the system does not
+// fit in shared memory (nullptr: both in shared memory)
 __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, const double* __restrict__ b,
                                                  const double* __restrict__ y, double* __restrict__ s,
-                                                 int32_t* __restrict__ path) {
+                                                 int32_t* __restrict__ path, double* gscr) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  double* B = reinterpret_cast<double*>(smraw);
+  const size_t sys = ls_batched_doubles(M, K) + csne_gram_doubles(K);
+  double* B = gscr ? gscr + (size_t)blockIdx.x * sys : reinterpret_cast<double*>(smraw);
   double* G = B + ls_batched_doubles(M, K);
-  double* rv = G + csne_gram_doubles(K);
+  double* rv = gscr ? reinterpret_cast<double*>(smraw) : G + csne_gram_doubles(K);
   double* sv = rv + M + 1;
   double* vn1 = sv + K + 9;
   double* vn2 = vn1 + K + 9;
@@ -130,13 +133,75 @@ __global__ void __launch_bounds__(128) ls_kernel(long long P, int M, int K, cons
 
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s, int32_t* path,
                               cudaStream_t stream) {
-  const size_t smem = sizeof(double) * (ls_batched_doubles(M, K) + csne_gram_doubles(K) + M + 1 + 4 * (K + 9)) +
-                      sizeof(LsShared) + sizeof(int) * (K + 2);
-  if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  long long blocks = P < 148 * 4 ? P : 148 * 4;
+  const size_t sys = ls_batched_doubles(M, K) + csne_gram_doubles(K);
+  const size_t vecs = sizeof(double) * (M + 1 + 4 * (K + 9)) + sizeof(LsShared) + sizeof(int) * (K + 2);
+  size_t smem = sizeof(double) * sys + vecs;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long blocks = P < 4LL * sms ? P : 4LL * sms;
+  // systems whose matrix and Gram exceed shared memory keep both in a
+  // stream-ordered global scratch (one per CTA); only the vectors stay shared
+  double* gscr = nullptr;
+  if (smem > 220 * 1024) {
+    smem = vecs;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gscr), sizeof(double) * sys * blocks, stream);
+    if (e != cudaSuccess) return e;
+  }
   cudaError_t e = cudaFuncSetAttribute(ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  ls_kernel<<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path);
+  if (e == cudaSuccess) {
+    ls_kernel<<<(int)blocks, 128, smem, stream>>>(P, M, K, b, y, s, path, gscr);
+    e = cudaGetLastError();
+  }
+  if (gscr) {
+    cudaError_t f = cudaFreeAsync(gscr, stream);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
+}
+
+// masks must be strictly increasing band indices < N (the reference's
+// Dictionary rows, transform.py:106-113): one thread per pixel row; any
+// violation sets kErrMask in the workspace error word, and every solver
+// kernel of the call then exits before reading a mask
+__global__ void validate_masks_kernel(long long P, int M, int N, const uint8_t* __restrict__ mask, int* err) {
+  int bad = 0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P; p += (long long)gridDim.x * blockDim.x) {
+    const uint8_t* row = mask + p * M;
+    int prev = -1;
+    for (int j = 0; j < M; ++j) {
+      const int v = row[j];
+      bad |= (v <= prev) | (v >= N);
+      prev = v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, kErrMask);
+}
+
+cudaError_t launch_validate_masks(long long P, int M, int N, const uint8_t* mask, int* err, int sms,
+                                  cudaStream_t stream) {
+  long long blocks = (P + 255) / 256;
+  if (blocks > 8LL * sms) blocks = 8LL * sms;
+  if (blocks < 1) blocks = 1;
+  validate_masks_kernel<<<(int)blocks, 256, 0, stream>>>(P, M, N, mask, err);
+  return cudaGetLastError();
+}
+
+// max_ij |(Psi^T Psi - I)_ij| of an N x N basis: one thread per entry, the
+// maximum by an atomic on the (non-negative) double's bits
+__global__ void basis_gram_dev_kernel(int N, const double* __restrict__ basis, unsigned long long* out) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.x * blockDim.x) {
+    const int i = idx / N, j = idx - i * N;
+    double s = 0.0;
+    for (int k = 0; k < N; ++k) s = fma(basis[(size_t)k * N + i], basis[(size_t)k * N + j], s);
+    double dev = fabs(s - (i == j ? 1.0 : 0.0));
+    if (dev != dev) dev = INFINITY;
+    atomicMax(out, (unsigned long long)__double_as_longlong(dev));
+  }
+}
+
+cudaError_t launch_basis_gram_dev(int N, const double* basis, unsigned long long* out, cudaStream_t stream) {
+  basis_gram_dev_kernel<<<(N * N + 255) / 256, 256, 0, stream>>>(N, basis, out);
   return cudaGetLastError();
 }
 

@@ -246,6 +246,7 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState<
 // epilogues and slot phase overlap the other's GEMMs on the DMMA pipe.
 template <int ALGO, int SL, int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
+  if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
   constexpr int CB = SL / 8;                  // 8-column blocks
   constexpr int MAXRB = (SL == 32) ? 2 : 4;   // row blocks per warp
   constexpr int NV = 2 * CB;                  // per-lane column partials
@@ -589,7 +590,8 @@ __global__ void prep_basis_kernel(const double* __restrict__ basis, int N, int N
 // Lipschitz constants of every pixel's A (fista), one warp per pixel, ahead
 // of the slot engine so that a refill never waits on the power iteration.
 __global__ void lipschitz_prepass_kernel(long long P, int M, const uint8_t* __restrict__ mask,
-                                         const double* __restrict__ u0, double* __restrict__ lip) {
+                                         const double* __restrict__ u0, double* __restrict__ lip, const int* err) {
+  if (*(volatile const int*)err & kErrMask) return;
   const int lane = threadIdx.x & 31;
   const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -600,8 +602,8 @@ __global__ void lipschitz_prepass_kernel(long long P, int M, const uint8_t* __re
 }
 
 cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
-                                     int sms, cudaStream_t stream) {
-  lipschitz_prepass_kernel<<<sms * 8, 256, 0, stream>>>(P, M, mask, u0, lip);
+                                     const int* err, int sms, cudaStream_t stream) {
+  lipschitz_prepass_kernel<<<sms * 8, 256, 0, stream>>>(P, M, mask, u0, lip, err);
   return cudaGetLastError();
 }
 
@@ -625,6 +627,7 @@ cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS,
 // scratch by the slot engine.  One warp per pixel, rows n = lane + 32 k.
 __global__ void __launch_bounds__(256) admm_zero_kernel(ConvexArgs a, long long* plist,
                                                         unsigned long long* plist_n) {
+  if (*(volatile const int*)a.err & kErrMask) return;
   __shared__ double syw[8][kMaxN];
   __shared__ uint8_t smw[8][kMaxN];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -760,11 +763,22 @@ size_t convex_smem_bytes(int algo, int Np, int M, int slots) {
 // CTA's tensor work instead of overlapping it: measured 15% slower (FISTA
 // 62.6 -> 73.2 ms, ADMM 103.7 -> 120.6 ms on 100k Salinas pixels;
 // epilogue cycles x5.6 per CTA; profiles/convex_slots_ab_r01.txt).
+// Systems whose 32-slot layout exceeds the 227 KB of one CTA (N = 224 with
+// M above ~116, i.e. sampling ratios above ~0.52) take the 16-slot engine, one
+// or two CTAs per SM; 0 = not even 16 slots fit (HCS_EINVAL).
 int convex_slots(int algo, int Np, int M) {
+  constexpr size_t kCta = 227 * 1024;
   int want = 32;
   if (const char* ov = getenv("HCS_CONVEX_SLOTS")) want = atoi(ov) == 16 ? 16 : 32;
   if (want == 16 && 2 * (convex_smem_bytes(algo, Np, M, 16) + 1024) > 228 * 1024) want = 32;
+  if (want == 32 && convex_smem_bytes(algo, Np, M, 32) > kCta) want = 16;
+  if (want == 16 && convex_smem_bytes(algo, Np, M, 16) > kCta) return 0;
   return want;
+}
+
+int convex_ctas_per_sm(int algo, int Np, int M, int slots) {
+  if (slots == 32) return 1;
+  return 2 * (convex_smem_bytes(algo, Np, M, 16) + 1024) <= 228 * 1024 ? 2 : 1;
 }
 
 template <int ALGO, int SL, int MAXT, int MINB>

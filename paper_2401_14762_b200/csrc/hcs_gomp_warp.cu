@@ -1,0 +1,628 @@
+// hcs_gomp_warp.cu -- warp-per-pixel gOMP with register-resident Householder QR.
+//
+// Reference: hypercs/solvers.py:248-297 (gomp), stop rule :115-127, y = 0
+// shortcut :145-152, non-finite failure :155-157; selection = argmax_k
+// (kernels.py:31-41); least squares = kernels.least_squares (kernels.py:44-67,
+// Householder QR + triangular solve).
+//
+// Why Householder and not normal equations: gOMP's second pass selects its G
+// atoms from A^T r where r is the residual of an (often exact) fit, i.e. from
+// roundoff.  Which noise columns win depends on the rounding statistics of the
+// least-squares solve: a QR solve leaves a component of size ~eps ||y|| in
+// range(A) that a refined normal-equations solve removes, and with it the
+// selection drifts towards columns outside the fitted set.  Measured on the
+// oracle (tools/gomp_rounding_study.py) and on the GPU (profiles/
+// gomp_ls_statistics_r02.txt): CSNE gives 2.5x the oracle's 1-ulp tie rate
+// and cube PSNR outside the oracle's 1-ulp band; Householder QR sits inside.
+//
+// Organisation: one warp per pixel, 8 independent warps per CTA (no CTA
+// barriers), pixels from a global atomic queue.  Per pass:
+//   * correlation p = A^T r: lanes over bands, Psi rows streamed from L2;
+//   * top-G by G warp argmax rounds (key = |p| bits, ties to the lowest index);
+//   * the columns of the least-squares systems are ordered [S | fills]: when
+//     |S| <= kappa the reference's second system top = argmax_k(scatter(s),
+//     kappa) is S plus the kappa - |S| lowest-index zero fills (checked after
+//     the fact), so ONE Householder QR of [S | fills] gives both solutions:
+//     LS(S) from its leading |S| x |S| block and LS(top) from the whole;
+//   * the QR: lanes own columns (column c in lane c's registers, up to 96
+//     rows), the reflector vector is broadcast through shared memory, each
+//     lane applies it to its own column (no cross-lane reductions); y is
+//     carried in lanes-over-rows form (Q^T y with a warp sum per reflector);
+//     a 33rd column is a "pre-column" handled lanes-over-rows the same way;
+//   * residual y - A x from the gathered columns (kept in shared memory),
+//     delta, stop rule.
+// Pixels outside the fast path (supports beyond 33 columns, a rank guard
+// min|R_ii| <= 1e-6 max|R_ii| where the reference's pivoted rank decision
+// could differ, non-finite intermediates) are handed to the CTA kernel
+// (hcs_greedy.cu, pivoted QR mode) through a spill list and solved there
+// from scratch.
+#include "hcs_internal.cuh"
+
+namespace hcs {
+
+constexpr int kWarpCols = 33;   // LS columns of the fast path: 32 lane columns + 1 pre-column
+constexpr int kGwWarps = 8;     // warps (pixels) per CTA
+
+struct GwLayout {
+  int ldc;                // leading dimension of the gathered columns (odd: conflict-free lane-column reads)
+  int orig, vb, r, y, xv, cb; // double offsets
+  int bytes_off;          // byte region offset (in doubles)
+  size_t bytes;           // per warp, 16-byte aligned
+};
+
+__host__ __device__ inline GwLayout gw_layout(int M) {
+  GwLayout L;
+  L.ldc = M | 1;
+  int o = 0;
+  L.orig = o; o += kWarpCols * L.ldc;
+  o = (o + 1) & ~1;
+  L.vb = o; o += kMaxN;       // reflector vector (MR) / dense x row / scatter scratch (N)
+  L.r = o; o += M;
+  L.y = o; o += M;
+  L.xv = o; o += 40;
+  L.cb = o; o += 80;          // back-substitution column buffers (2 x 40)
+  L.bytes_off = o;
+  size_t b = sizeof(double) * (size_t)o;
+  b += 128 + 64 + 64;         // mask (<= 96 B, padded), column list (40 B), bitmaps / flags
+  L.bytes = (b + 15) & ~(size_t)15;
+  return L;
+}
+
+struct GwBytes {
+  uint8_t msk[128];
+  uint8_t cols[64];
+  uint32_t supp[8];
+  uint32_t sel[8];
+};
+
+__device__ __forceinline__ unsigned long long gw_key(double v) {
+  // argmax_k order (stable argsort of -|v|): larger |v| first, NaN last; 0 = taken
+  const double a = fabs(v);
+  if (a != a) return 1ull;
+  return (unsigned long long)__double_as_longlong(a) + 2ull;
+}
+
+__device__ __forceinline__ void gw_trace(const Stats& st, long long pid, int& ncall, const uint32_t* bm, int lane) {
+  if (st.trace != nullptr && ncall < st.trace_calls && lane < 4) {
+    uint64_t* dst = st.trace + ((size_t)pid * st.trace_calls + ncall) * 4;
+    dst[lane] = (uint64_t)bm[2 * lane] | ((uint64_t)bm[2 * lane + 1] << 32);
+  }
+  ++ncall;
+}
+
+// sorted index list of a 256-bit bitmap (one warp); returns the count
+__device__ __forceinline__ int bitmap_to_list_warp(const uint32_t* bm, uint8_t* list, int lane) {
+  int base = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t word = bm[e];
+    if ((word >> lane) & 1u) list[base + __popc(word & ((1u << lane) - 1u))] = (uint8_t)(32 * e + lane);
+    base += __popc(word);
+  }
+  __syncwarp();
+  return base;
+}
+
+// ---------------------------------------------------------------- QR passes
+// a[MR]: this lane's column (rows 0..MR).  Loops over rows >= j start at a
+// runtime chunk (4 rows) but must index a[] statically: a switch on the first
+// chunk falls through an unrolled sequence of per-chunk bodies (Duff's
+// device; nvcc emits one indexed branch).  Chunks past MR compile to nothing.
+#define GW_CASES(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) \
+  X(12) X(13) X(14) X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23)
+
+template <int MR, int CB>
+__device__ __forceinline__ void gw_dot_chunk(const double (&a)[MR], const double2* v2, double (&d)[4]) {
+  if constexpr (4 * CB + 3 < MR) {
+    const double2 va = v2[2 * CB], vc = v2[2 * CB + 1];
+    d[0] = fma(va.x, a[4 * CB], d[0]);
+    d[1] = fma(va.y, a[4 * CB + 1], d[1]);
+    d[2] = fma(vc.x, a[4 * CB + 2], d[2]);
+    d[3] = fma(vc.y, a[4 * CB + 3], d[3]);
+  }
+}
+
+template <int MR, int CB>
+__device__ __forceinline__ void gw_upd_chunk(double (&a)[MR], const double2* v2, double f) {
+  if constexpr (4 * CB + 3 < MR) {
+    const double2 va = v2[2 * CB], vc = v2[2 * CB + 1];
+    a[4 * CB] = fma(-f, va.x, a[4 * CB]);
+    a[4 * CB + 1] = fma(-f, va.y, a[4 * CB + 1]);
+    a[4 * CB + 2] = fma(-f, vc.x, a[4 * CB + 2]);
+    a[4 * CB + 3] = fma(-f, vc.y, a[4 * CB + 3]);
+  }
+}
+
+template <int MR, int CB>
+__device__ __forceinline__ void gw_copy_chunk(const double (&a)[MR], double2* v2) {
+  if constexpr (4 * CB + 3 < MR) {
+    v2[2 * CB] = make_double2(a[4 * CB], a[4 * CB + 1]);
+    v2[2 * CB + 1] = make_double2(a[4 * CB + 2], a[4 * CB + 3]);
+  }
+}
+
+// d = sum_{rows >= 4 (j / 4)} v_i a_i  (v is zero on the rows below j)
+template <int MR>
+__device__ __forceinline__ double gw_dot(const double (&a)[MR], const double* vb, int j) {
+  double d[4] = {0.0, 0.0, 0.0, 0.0};
+  const double2* v2 = reinterpret_cast<const double2*>(vb);
+  switch (j >> 2) {
+#define GW_DOT_CASE(k) case k: gw_dot_chunk<MR, k>(a, v2, d);
+    GW_CASES(GW_DOT_CASE)
+#undef GW_DOT_CASE
+    default: break;
+  }
+  return (d[0] + d[1]) + (d[2] + d[3]);
+}
+
+// a_i -= f v_i on the rows >= 4 (j / 4)
+template <int MR>
+__device__ __forceinline__ void gw_update(double (&a)[MR], const double* vb, int j, double f) {
+  const double2* v2 = reinterpret_cast<const double2*>(vb);
+  switch (j >> 2) {
+#define GW_UPD_CASE(k) case k: gw_upd_chunk<MR, k>(a, v2, f);
+    GW_CASES(GW_UPD_CASE)
+#undef GW_UPD_CASE
+    default: break;
+  }
+}
+
+// the owner's column, rows >= 4 (j / 4), into vb
+template <int MR>
+__device__ __forceinline__ void gw_copy(const double (&a)[MR], double* vb, int j) {
+  double2* v2 = reinterpret_cast<double2*>(vb);
+  switch (j >> 2) {
+#define GW_CPY_CASE(k) case k: gw_copy_chunk<MR, k>(a, v2);
+    GW_CASES(GW_CPY_CASE)
+#undef GW_CPY_CASE
+    default: break;
+  }
+}
+
+// Householder QR of the K gathered columns (orig, our column order) and
+// Q^T y.  Lanes own columns e + lane (e = K - 32 pre-columns, 0 or 1);
+// returns in every lane: its column's R part in a[0..], its diagonal in
+// rdiag; yw (lanes over rows) = Q^T y; beta0 = R_00 of the pre-column.
+// Per reflector j: the column (the owner lane's registers, or the
+// pre-column from orig) goes to vb; every lane reads xnorm^2 = sum_{i>j} v_i^2
+// (lanes over rows + warp sum) and alpha = v_j and forms beta, g = 1 /
+// (beta (beta - alpha)) (LAPACK dlarfg's reflector, unscaled:
+// H c = c - g (v^T c) v with v = [alpha - beta; x]); then each lane applies H
+// to its own column and the warp to y.
+template <int MR>
+__device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&yw)[MR / 32], double& beta0,
+                                      const double* orig, int ldc, double* vb, int K, int M, int lane) {
+  const int e = K > 32 ? K - 32 : 0;
+  const int myc = e + lane;
+#pragma unroll
+  for (int i = 0; i < MR; ++i) a[i] = (myc < K && i < M) ? orig[myc * ldc + i] : 0.0;
+  rdiag = 0.0;
+  beta0 = 0.0;
+  for (int j = 0; j < K; ++j) {
+    const int owner = j - e;   // < 0: the pre-column (column 0, lanes over rows)
+    if (owner < 0) {
+#pragma unroll
+      for (int q = 0; q < MR / 32; ++q) {
+        const int row = lane + 32 * q;
+        vb[row] = row < M ? orig[row] : 0.0;
+      }
+    } else if (lane == owner) {
+      gw_copy<MR>(a, vb, j);
+    }
+    __syncwarp();
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < MR / 32; ++q) {
+      const int row = lane + 32 * q;
+      if (row > j && row < M) part = fma(vb[row], vb[row], part);
+    }
+    const double xn2 = warp_sum(part);
+    const double al = vb[j];
+    double g = 0.0, amb = 0.0, beta = al;
+    if (xn2 != 0.0) {
+      beta = -copysign(sqrt(fma(al, al, xn2)), al);
+      amb = al - beta;
+      g = 1.0 / (beta * (beta - al));
+    }
+    if (owner < 0) beta0 = beta;
+    else if (lane == owner) rdiag = beta;
+    __syncwarp();   // every lane has read v_j
+    {
+      const int j0 = j & ~3;   // v: rows j0 .. j-1 of the first chunk read -> 0, row j -> alpha - beta
+      if (lane <= j - j0) vb[j0 + lane] = (j0 + lane == j) ? amb : 0.0;
+    }
+    __syncwarp();
+    double py = 0.0;
+#pragma unroll
+    for (int q = 0; q < MR / 32; ++q) {
+      const int row = lane + 32 * q;
+      if (row >= j && row < M) py = fma(vb[row], yw[q], py);
+    }
+    const double f = gw_dot<MR>(a, vb, j) * g;
+    gw_update<MR>(a, vb, j, f);
+    const double fy = warp_sum(py) * g;
+#pragma unroll
+    for (int q = 0; q < MR / 32; ++q) {
+      const int row = lane + 32 * q;
+      if (row >= j && row < M) yw[q] = fma(-fy, vb[row], yw[q]);
+    }
+    __syncwarp();   // vb is rewritten by the next owner
+  }
+}
+
+// Back substitution R x = z, column-oriented as LAPACK's dtrsv ('U', 'N'):
+// for c = K-1 .. 0: x_c = z_c / R_cc, then z_i -= R_ic x_c for i < c.
+// Column c of R is lane (c - e)'s register column, rows 0..c-1, staged through
+// shared memory (cbuf, two 40-double buffers) once per step.  Solves the full
+// system (xt) and the leading s x s block (xs, the LS(S) prefix) together.
+// Lane L receives x of column e + L; x0t / x0s: the pre-column's.
+template <int MR>
+__device__ __forceinline__ void gw_solve(const double (&a)[MR], double rdiag, const double (&yw)[MR / 32],
+                                         double beta0, int K, int s, int lane, double* cbuf, double& xt, double& xs,
+                                         double& x0t, double& x0s) {
+  const int e = K > 32 ? K - 32 : 0;
+  double zt0 = yw[0], zt1 = MR > 32 ? yw[MR > 32 ? 1 : 0] : 0.0;   // rows lane, lane + 32
+  double zs0 = zt0, zs1 = zt1;
+  xt = 0.0;
+  xs = 0.0;
+  x0t = 0.0;
+  x0s = 0.0;
+  for (int c = K - 1; c >= 0; --c) {
+    double* cb = cbuf + (c & 1) * 40;
+    const int owner = c - e;   // < 0: the pre-column (c = 0), no entries above the diagonal
+    if (owner >= 0 && lane == owner) {
+#pragma unroll
+      for (int i = 0; i < kWarpCols && i < MR; ++i)
+        if (i < c) cb[i] = a[i];
+    }
+    const double rcc = owner >= 0 ? __shfl_sync(0xffffffffu, rdiag, owner & 31) : beta0;
+    const double zct = __shfl_sync(0xffffffffu, (c >> 5) ? zt1 : zt0, c & 31);
+    const double zcs = __shfl_sync(0xffffffffu, (c >> 5) ? zs1 : zs0, c & 31);
+    const double vt = zct / rcc;
+    const double vs = c < s ? zcs / rcc : 0.0;
+    if (owner < 0) {
+      x0t = vt;
+      x0s = vs;
+    } else if (lane == owner) {
+      xt = vt;
+      xs = vs;
+    }
+    __syncwarp();
+    if (lane < c) {   // rows i < c <= 32 live in slot 0
+      const double r = cb[lane];
+      zt0 = fma(-r, vt, zt0);
+      if (c < s) zs0 = fma(-r, vs, zs0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+
+template <int MR>
+__global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs a, GwSpill sp) {
+  if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int N = a.N, M = a.M;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const GwLayout L = gw_layout(M);
+  double* S = reinterpret_cast<double*>(smraw + (size_t)warp * L.bytes);
+  double* orig = S + L.orig;
+  double* vb = S + L.vb;
+  double* rs = S + L.r;
+  double* ys = S + L.y;
+  double* xv = S + L.xv;
+  GwBytes& gb = *reinterpret_cast<GwBytes*>(S + L.bytes_off);
+  const int kappa = a.prm.kappa, G = a.prm.G;
+  const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+  constexpr int Q = MR / 32;
+
+  for (;;) {
+    long long pid = 0;
+    if (lane == 0) pid = (long long)atomicAdd(a.counter, 1ull);
+    pid = __shfl_sync(0xffffffffu, pid, 0);
+    if (pid >= a.P) break;
+    // ---- load the pixel ---------------------------------------------------
+    int nz = 0, bad = 0;
+    for (int j = lane; j < M; j += 32) {
+      const double v = a.y[pid * M + j];
+      ys[j] = v;
+      rs[j] = v;
+      gb.msk[j] = a.mask[pid * M + j];
+      nz |= (v != 0.0);
+      bad |= !isfinite(v);
+    }
+    if (lane < 8) gb.supp[lane] = 0u;
+    const long long t0 = now_ns();
+    nz = __any_sync(0xffffffffu, nz);
+    bad = __any_sync(0xffffffffu, bad);
+    __syncwarp();
+    if (!nz || bad) {   // y == 0 shortcut; non-finite y: scipy raises ValueError (kernels.py:61)
+      if (bad && lane == 0) atomicOr(a.err, 1);
+      for (int n = lane; n < N; n += 32) a.x_out[pid * N + n] = 0.0;
+      if (lane == 0) {
+        a.st.iterations[pid] = 0;
+        a.st.converged[pid] = bad ? 0 : 1;
+        a.st.final_delta[pid] = bad ? NaN : 0.0;
+        a.st.failed_at[pid] = -1;
+        if (a.st.trace_len) a.st.trace_len[pid] = 0;
+        if (a.st.elapsed) a.st.elapsed[pid] = 0.0;
+        if (a.st.work) a.st.work[pid] = 0.0;
+      }
+      continue;
+    }
+    double delta = 1.0;
+    int iters = 0, ncall = 0, kx = 0;
+    bool converged = false, failed = false, spill = false;
+    double work = 0.0;
+    for (;;) {
+      // ---- stop rule before the pass (solvers.py:115-127) -------------------
+      int dec = 0;
+      if (lane == 0) dec = stop_decision(delta, iters, t0, a.prm);
+      dec = __shfl_sync(0xffffffffu, dec, 0);
+      if (dec != kContinue) { converged = dec == kConverged; break; }
+      // ---- correlation p = A^T r: lanes over bands, Psi rows from L2 --------
+      double p[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) p[c] = 0.0;
+      {
+        int j = 0;
+        for (; j + 1 < M; j += 2) {
+          const double r0 = rs[j], r1 = rs[j + 1];
+          const double* row0 = a.basis + (size_t)gb.msk[j] * N + lane;
+          const double* row1 = a.basis + (size_t)gb.msk[j + 1] * N + lane;
+          double b0[8], b1[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            b0[c] = lane + 32 * c < N ? __ldg(row0 + 32 * c) : 0.0;
+            b1[c] = lane + 32 * c < N ? __ldg(row1 + 32 * c) : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) p[c] = fma(b1[c], r1, fma(b0[c], r0, p[c]));
+        }
+        if (j < M) {
+          const double r0 = rs[j];
+          const double* row0 = a.basis + (size_t)gb.msk[j] * N + lane;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (lane + 32 * c < N) p[c] = fma(__ldg(row0 + 32 * c), r0, p[c]);
+        }
+      }
+      // ---- top-G (argmax_k, kernels.py:31-41) by G warp argmax rounds ---------
+      {
+        unsigned long long key[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) key[c] = lane + 32 * c < N ? gw_key(p[c]) : 0ull;
+        uint32_t selw = 0u;   // lane's word: bit c <-> index lane + 32 c
+        for (int g = 0; g < G; ++g) {
+          unsigned long long bk = 0ull;
+          int bi = 1 << 30;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (key[c] > bk) { bk = key[c]; bi = lane + 32 * c; }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ok > bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+          }
+          if ((bi & 31) == lane) {
+            const int c = bi >> 5;
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc)
+              if (cc == c) key[cc] = 0ull;
+            selw |= 1u << c;
+          }
+        }
+        // transpose to index bitmaps: word w bit b <-> index 32 w + b
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t m = __ballot_sync(0xffffffffu, (selw >> c) & 1u);
+          if (lane == c) gb.sel[c] = m;
+        }
+        __syncwarp();
+        gw_trace(a.st, pid, ncall, gb.sel, lane);
+      }
+      // ---- support union, outgrowth break ------------------------------------
+      uint32_t sw = lane < 8 ? (gb.supp[lane] | gb.sel[lane]) : 0u;
+      const int ks = __reduce_add_sync(0xffffffffu, __popc(sw));
+      work += 2.0 * N * M;   // correlation
+      if (ks > M) break;     // keep the last iterate, no count (solvers.py:274-276)
+      __syncwarp();
+      if (lane < 8) gb.supp[lane] = sw;
+      __syncwarp();
+      if (ks > kWarpCols || kappa > kWarpCols) { spill = true; break; }
+      // ---- column order [S | fills] ------------------------------------------
+      // S sorted, then (ks <= kappa) the kappa - ks lowest indices outside S
+      int K;
+      {
+        int base = 0, fbase = ks, fill_need = ks <= kappa ? kappa - ks : 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const uint32_t word = gb.supp[w];
+          const bool on = (word >> lane) & 1u;
+          const int idx = 32 * w + lane;
+          if (on) gb.cols[base + __popc(word & ((1u << lane) - 1u))] = (uint8_t)idx;
+          base += __popc(word);
+          const bool fz = !on && idx < N;
+          const uint32_t fm = __ballot_sync(0xffffffffu, fz);
+          const int rk = __popc(fm & ((1u << lane) - 1u));
+          if (fz && rk < fill_need) gb.cols[fbase + rk] = (uint8_t)idx;
+          const int take = __popc(fm) < fill_need ? __popc(fm) : fill_need;
+          fbase += take;
+          fill_need -= take;
+        }
+        K = ks <= kappa ? kappa : ks;
+      }
+      __syncwarp();
+      double xt = 0.0, x0t = 0.0;
+      bool second = false;
+      for (int round = 0; round < 2; ++round) {
+        // ---- gather the K columns at the measured rows (L2 -> shared) ---------
+        for (int c = 0; c < K; ++c) {
+          const double* col = a.basis_t + (size_t)gb.cols[c] * N;
+          for (int i = lane; i < M; i += 32) cp_async8(orig + c * L.ldc + i, col + gb.msk[i]);
+        }
+        cp_async_wait_all();
+        __syncwarp();
+        double acol[MR];
+        double rdiag, beta0;
+        double yw[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) yw[q] = lane + 32 * q < M ? ys[lane + 32 * q] : 0.0;
+        gw_qr<MR>(acol, rdiag, yw, beta0, orig, L.ldc, vb, K, M, lane);
+        // rank guard on the diagonal of R (see header)
+        {
+          const int e = K > 32 ? K - 32 : 0;
+          const double dl = (e + lane < K) ? fabs(rdiag) : 0.0;
+          double dmax = dl, dmin = (e + lane < K) ? dl : INFINITY;
+          if (e) { dmax = fmax(dmax, fabs(beta0)); dmin = fmin(dmin, fabs(beta0)); }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+            dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+          }
+          if (!(dmin > 1e-6 * dmax) || K > M) { spill = true; break; }
+        }
+        const int s = (!second && ks <= kappa) ? ks : 0;
+        double xs, x0s;
+        gw_solve<MR>(acol, rdiag, yw, beta0, K, s, lane, S + L.cb, xt, xs, x0t, x0s);
+        if (second) break;   // second round done: xt is LS(top)
+        // the top call: argmax_k(scatter(LS(S)), kappa) over all N bands.
+        // |S| <= kappa: the predicted top [S | fills] is the real one iff every
+        // LS(S) coefficient is nonzero (zeros tie with the fills, NaN ranks
+        // last); otherwise (or |S| > kappa) the exact warp top-k selects it and
+        // a second QR solves on those columns
+        const int e = K > 32 ? K - 32 : 0;
+        const int myc = e + lane;
+        bool general = ks > kappa;
+        double sv = xs, sv0 = x0s;
+        if (general) {
+          sv = xt;      // |S| > kappa: the first round solved S itself
+          sv0 = x0t;
+        } else {
+          bool zero = (myc < s) && !(xs != 0.0 && xs == xs);
+          if (e && lane == 0) zero |= !(x0s != 0.0 && x0s == x0s);
+          general = __any_sync(0xffffffffu, zero);
+        }
+        if (general) {
+          const int ns = ks;   // the S columns are cols[0 .. ks)
+          for (int n = lane; n < N; n += 32) vb[n] = 0.0;
+          __syncwarp();
+          if (e && lane == 0) vb[gb.cols[0]] = sv0;
+          if (myc < ns) vb[gb.cols[myc]] = sv;
+          __syncwarp();
+          warp_topk(vb, N, kappa, gb.sel);
+          __syncwarp();
+          gw_trace(a.st, pid, ncall, gb.sel, lane);
+          bitmap_to_list_warp(gb.sel, gb.cols, lane);
+          K = kappa;
+          second = true;
+          __syncwarp();
+          continue;
+        }
+        {
+          // trace record of the top call: the bitmap of [S | fills]
+          uint32_t tw = 0u;
+          for (int c = 0; c < K; ++c) {
+            const int idx = gb.cols[c];
+            if ((idx >> 5) == lane) tw |= 1u << (idx & 31);
+          }
+          if (lane < 8) gb.sel[lane] = tw;
+          __syncwarp();
+          gw_trace(a.st, pid, ncall, gb.sel, lane);
+        }
+        break;
+      }
+      if (spill) break;
+      work += ls_flops(M, ks) + ls_flops(M, kappa);
+      // ---- new iterate, residual, delta (solvers.py:285-290) ------------------
+      kx = K;
+      {
+        const int e = K > 32 ? K - 32 : 0;
+        if (e + lane < K) xv[e + lane] = xt;
+        if (e && lane == 0) xv[0] = x0t;
+      }
+      __syncwarp();
+      double part = 0.0;
+      int nf = 0;
+      for (int i = lane; i < M; i += 32) {
+        double acc0 = 0.0, acc1 = 0.0;
+        int c = 0;
+        for (; c + 1 < K; c += 2) {
+          acc0 = fma(orig[c * L.ldc + i], xv[c], acc0);
+          acc1 = fma(orig[(c + 1) * L.ldc + i], xv[c + 1], acc1);
+        }
+        if (c < K) acc0 = fma(orig[c * L.ldc + i], xv[c], acc0);
+        const double rn = ys[i] - (acc0 + acc1);
+        const double d = rn - rs[i];
+        part = fma(d, d, part);
+        rs[i] = rn;
+      }
+      for (int c = lane; c < K; c += 32) nf |= !isfinite(xv[c]);
+      delta = sqrt(warp_sum(part));
+      work += 2.0 * M * K;
+      nf = __any_sync(0xffffffffu, nf);
+      __syncwarp();
+      ++iters;
+      if (nf || !isfinite(delta)) { failed = true; break; }
+    }
+    if (spill) {
+      if (lane == 0) {
+        const unsigned long long k = atomicAdd(sp.count, 1ull);
+        sp.list[k] = pid;
+      }
+      __syncwarp();
+      continue;
+    }
+    // ---- results: dense x row through shared memory -------------------------------
+    for (int n = lane; n < N; n += 32) vb[n] = 0.0;
+    __syncwarp();
+    if (!failed)
+      for (int c = lane; c < kx; c += 32) vb[gb.cols[c]] = xv[c];
+    __syncwarp();
+    for (int n = lane; n < N; n += 32) a.x_out[pid * N + n] = vb[n];
+    if (lane == 0) {
+      a.st.iterations[pid] = failed ? 0 : iters;
+      a.st.converged[pid] = converged ? 1 : 0;
+      a.st.final_delta[pid] = failed ? NaN : delta;
+      a.st.failed_at[pid] = failed ? iters : -1;
+      if (a.st.trace_len) a.st.trace_len[pid] = ncall;
+      if (a.st.elapsed) a.st.elapsed[pid] = 1e-9 * (double)(now_ns() - t0);
+      if (a.st.work) a.st.work[pid] = work;
+    }
+    __syncwarp();
+  }
+}
+
+bool gomp_warp_supported(int N, int M, int kappa) { return M <= 96 && kappa <= kWarpCols && N <= kMaxN && M >= 1; }
+
+size_t gomp_warp_smem(int M, int* warps) {
+  const GwLayout L = gw_layout(M);
+  int w = kGwWarps;
+  while (w > 1 && L.bytes * w > 227 * 1024) --w;
+  *warps = w;
+  return L.bytes * w;
+}
+
+template <int MR>
+static cudaError_t launch_gw_t(const GreedyArgs& args, const GwSpill& sp, int grid, int warps, size_t smem,
+                               cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(gomp_warp_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gomp_warp_kernel<MR><<<grid, 32 * warps, smem, stream>>>(args, sp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, cudaStream_t stream) {
+  int warps = 0;
+  const size_t smem = gomp_warp_smem(args.M, &warps);
+  long long grid = sms;
+  const long long need = (args.P + warps - 1) / warps;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  if (args.M <= 32) return launch_gw_t<32>(args, sp, (int)grid, warps, smem, stream);
+  if (args.M <= 64) return launch_gw_t<64>(args, sp, (int)grid, warps, smem, stream);
+  return launch_gw_t<96>(args, sp, (int)grid, warps, smem, stream);
+}
+
+}  // namespace hcs

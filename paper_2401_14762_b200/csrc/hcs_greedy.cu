@@ -132,6 +132,7 @@ __device__ __forceinline__ int bitmap_to_list(const uint32_t* bm, uint8_t* list)
 
 template <int ALGO>
 __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a) {
+  if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
   extern __shared__ __align__(16) unsigned char smraw[];
   const int N = a.N, M = a.M;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -180,6 +181,18 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
     ls_shared = shared_b;
     ls_b = B;
     ls_ok = false;
+    if (a.ls_mode == 1) {
+      // pivoted Householder QR (the reference's algorithm), row-major B with y as column K
+      const int ldp = (K + 1) | 1;
+      for (int idx = tid; idx < M * (K + 1); idx += nt) {
+        const int rr = idx / (K + 1), c = idx - rr * (K + 1);
+        B[rr * ldp + c] = (c < K) ? __ldg(a.basis + (size_t)msk[rr] * N + cols[c]) : ys[rr];
+      }
+      __syncthreads();
+      ls_solve(B, ldp, M, K, sv, sc);
+      GMARK(9);
+      return;
+    }
     const int ldb = csne_ld(M);                  // column-major; y is column K
     const int nc = csne_cols(K);
     // asynchronous gather (cp.async, L2 -> shared, no register staging): warp w
@@ -243,8 +256,13 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   for (;;) {
     if (tid == 0) { g.pid = (long long)atomicAdd(a.counter, 1ull); g.ctr = 1; }
     __syncthreads();
-    const long long pid = g.pid;
-    if (pid >= a.P) break;
+    long long pid = g.pid;
+    if (a.plist) {
+      if ((unsigned long long)pid >= *a.plist_n) break;
+      pid = a.plist[pid];
+    } else if (pid >= a.P) {
+      break;
+    }
     // ---- load the pixel -----------------------------------------------------
     int nz = 0, bad = 0;
     for (int j = tid; j < M; j += nt) {

@@ -41,6 +41,21 @@ struct GreedyArgs {
   int* err;
   double* gscratch;      // per-CTA global LS scratch (systems beyond the shared-memory size)
   const double* basis_t;   // Psi transposed (basis_t[c N + r] = Psi[r][c]): column gathers read one column
+  // least-squares method: 0 = CSNE fast path with the guarded pivoted-QR
+  // fallback; 1 = pivoted Householder QR always (LAPACK dlaqp2 restatement,
+  // the reference's own algorithm: its rounding statistics decide gOMP's
+  // noise-level selections, tools/gomp_rounding_study.py)
+  int ls_mode = 0;
+  // optional pixel list (the pixels the warp-per-pixel gOMP kernel spilled):
+  // the CTA kernel then works on plist[0 .. *plist_n) instead of 0 .. P-1
+  const long long* plist = nullptr;
+  const unsigned long long* plist_n = nullptr;
+};
+
+// spill list of the warp-per-pixel gOMP kernel
+struct GwSpill {
+  unsigned long long* count;
+  long long* list;
 };
 
 // hcs_convex.cu
@@ -49,8 +64,9 @@ size_t convex_smem_bytes(int algo, int Np, int M, int slots);
 cudaError_t launch_admm_zero(const ConvexArgs& args, long long* plist, unsigned long long* plist_n, int sms,
                              cudaStream_t stream);
 int convex_slots(int algo, int Np, int M);
+int convex_ctas_per_sm(int algo, int Np, int M, int slots);
 cudaError_t launch_lipschitz_prepass(long long P, int M, const uint8_t* mask, const double* u0, double* lip,
-                                     int sms, cudaStream_t stream);
+                                     const int* err, int sms, cudaStream_t stream);
 cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS, double* fragT, double* u0,
                               int slots, cudaStream_t stream);
 // hcs_greedy.cu
@@ -60,7 +76,13 @@ int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap);
 size_t greedy_ls_doubles(int M);
 cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, cudaStream_t stream);
 int greedy_blocks_per_sm(int algo, int M, size_t smem);
+// hcs_gomp_warp.cu
+bool gomp_warp_supported(int N, int M, int kappa);
+cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, cudaStream_t stream);
 // hcs_batched.cu
+cudaError_t launch_basis_gram_dev(int N, const double* basis, unsigned long long* out, cudaStream_t stream);
+cudaError_t launch_validate_masks(long long P, int M, int N, const uint8_t* mask, int* err, int sms,
+                                  cudaStream_t stream);
 cudaError_t launch_batched_ls(long long P, int M, int K, const double* b, const double* y, double* s,
                               int32_t* path, cudaStream_t stream);
 cudaError_t launch_argmax_k(long long P, int n, const double* v, int k, int32_t* idx, cudaStream_t stream);

@@ -157,6 +157,12 @@ class DeviceBatch:
     trace_len: object = None
     workspace: object = None
     launches: int = 0        # kernels this call launched (prep + solver)
+    algorithm: str = ""
+
+    def error_flag(self):
+        """The device word hcs_recover_status reads (int32 view into the
+        workspace; non-zero after a non-finite measurement)."""
+        return self.workspace[8:12].view(__import__("torch").int32)
 
     def check_status(self, stream=None):
         """Raise ValueError where the reference raises on non-finite input (syncs)."""
@@ -182,6 +188,10 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
     f64 = dict(dtype=torch.float64, device=dev)
     if out is not None and tuple(out.x.shape) == (P, n) and trace_calls == 0:
         workspace = out.workspace if workspace is None else workspace
+        if out.algorithm != algorithm:
+            # fields only some solvers write (admm_gap: admm; lipschitz: fista)
+            out.admm_gap.fill_(math.nan)
+            out.lipschitz.fill_(math.nan)
     else:
         out = None
     out = out or DeviceBatch(
@@ -215,7 +225,8 @@ def solve_batch(algorithm, y, masks, basis, config, trace_calls=0, stream=None, 
     nat.check(lib.hcs_recover(algo, P, n, m, nat.ptr(basis), nat.ptr(y), nat.ptr(masks), prm, nat.ptr(out.x),
                               st, nat.ptr(workspace), workspace.numel(), sh))
     out.workspace = workspace
-    out.launches = (3 if algorithm in CONVEX_SOLVERS else 2) if P > 0 else 0   # convex: prep + (lipschitz | zero pass) + engine; greedy: basis transpose + engine
+    out.algorithm = algorithm
+    out.launches = lib.hcs_recover_launches(algo, n, m, prm) if P > 0 else 0
     if check_status:
         out.check_status(stream)
     return out
@@ -411,6 +422,14 @@ def _chunk_view(b, p0, p1):
                        work=b.work[p0:p1])
 
 
+def _raise_error_word(flag):
+    """ValueErrors of the workspace error word (hcs_recover_status)."""
+    if flag & 2:
+        raise ValueError("mask entries must be strictly increasing band indices < N")
+    if flag:
+        raise ValueError("array must not contain infs or NaNs")
+
+
 def _recover_host(algorithm, y_host, dictionary, config, x_host, chunk_pixels, stream):
     """Host buffers in and out, pipelined in pixel chunks: the H2D copy of
     chunk k+1 and the D2H copy of chunk k-1 run on their own streams while
@@ -496,10 +515,10 @@ def _recover_host(algorithm, y_host, dictionary, config, x_host, chunk_pixels, s
         drain(len(bounds) - 1)
     for s in (s_in, s_c0, s_c1, s_out):
         main.wait_stream(s)
-    if bounds and int(errs.max().item()):   # the flag hcs_recover_status reads, per chunk
-        raise ValueError("array must not contain infs or NaNs")
+    if bounds:   # the error word hcs_recover_status reads, per chunk
+        _raise_error_word(int(((errs & 2).amax() | (errs & 1).amax()).item()))
     full.workspace = ws[0] if ws else None
-    full.launches = sum((3 if algorithm in CONVEX_SOLVERS else 2) for _ in bounds)
+    full.launches = sum(lib.hcs_recover_launches(algo, n, m, config.to_native()) for _ in bounds)
     return full
 
 
@@ -547,6 +566,22 @@ def recover_cube(measurements, dictionary, config, algorithm, jobs=1, stream=Non
     if algorithm == "admm":
         dictionary.admm_factor(config.alpha)
     config.to_native()   # config errors before any device work
+    if stream is not None:
+        # everything below (solve, error flags, statistics reductions, the
+        # copies) is ordered on the caller's stream
+        with torch.cuda.stream(stream):
+            return _recover_cube_on_stream(meas, is_torch, on_device, dictionary, config, algorithm, out,
+                                           chunk_pixels, x_dim, y_dim, m, stream)
+    return _recover_cube_on_stream(meas, is_torch, on_device, dictionary, config, algorithm, out, chunk_pixels,
+                                   x_dim, y_dim, m, None)
+
+
+def _recover_cube_on_stream(meas, is_torch, on_device, dictionary, config, algorithm, out, chunk_pixels, x_dim,
+                            y_dim, m, stream):
+    import time
+    import torch
+    P = x_dim * y_dim
+    n = dictionary.n
     t0 = time.perf_counter()
     if on_device:
         if out is not None:

@@ -293,3 +293,42 @@ CUBES = {
 def generate_named(name, seed=0, x_range=None, workers=1):
     spec = dict(CUBES[name])
     return generate(seed=seed, x_range=x_range, workers=workers, **spec)
+
+
+def _strided_job(args):
+    """Pixels of one tile whose global flat index is a multiple of `stride`."""
+    n_pix, n, seed, i, j, bx, by, y_dim, stride = args
+    c, f, mk, yy = _tile(n_pix, n, dct_basis(n), seed)
+    t = np.arange(n_pix)
+    p = (i * bx + t // by) * y_dim + j * by + t % by          # global x-major index
+    keep = np.flatnonzero(p % stride == 0)
+    return p[keep], c[keep], f[keep], mk[keep], yy[keep]
+
+
+def generate_strided(name, stride=97, seed=0, workers=1):
+    """Every `stride`-th pixel (global x-major index p with p % stride == 0) of
+    a named cube, bit-identical to the same pixels of `generate_named` --
+    the fixed deterministic subset the CPU baseline is timed on (SURVEY.md
+    §8(d): "every 97th pixel").  Tiles are generated whole (the random stream
+    is per tile) in a process pool and reduced to their sampled pixels.
+    Returns a SyntheticCube of shape (S, 1) in increasing p order; its
+    ``seeds`` holds the tile seeds and ``pixel_index`` the global indices."""
+    spec = dict(CUBES[name])
+    x_dim, y_dim, n = spec["x_dim"], spec["y_dim"], spec["n"]
+    tx, ty = spec.get("tiles", (1, 1))
+    bx, by = x_dim // tx, y_dim // ty
+    jobs = [(bx * by, n, seed + ty * i + j, i, j, bx, by, y_dim, stride) for i in range(tx) for j in range(ty)]
+    if workers > 1 and len(jobs) > 1:
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(max_workers=min(workers, len(jobs))) as pool:
+            parts = list(pool.map(_strided_job, jobs))
+    else:
+        parts = [_strided_job(jb) for jb in jobs]
+    p = np.concatenate([pt[0] for pt in parts])
+    order = np.argsort(p, kind="stable")
+    cat = [np.concatenate([pt[k] for pt in parts])[order] for k in range(1, 5)]
+    cube = SyntheticCube(basis=dct_basis(n), coeffs=cat[0], spectra=cat[1], masks=cat[2],
+                         y=np.ascontiguousarray(cat[3]), shape=(len(p), 1),
+                         seeds=tuple(jb[2] for jb in jobs))
+    cube.pixel_index = p[order]
+    return cube

@@ -55,7 +55,7 @@ def test_sass_uses_fp64_tensor_cores(lib_path):
 def test_host_only_entry_points(lib_path):
     from paper_2401_14762_b200 import _native
     lib = _native.load(lib_path)
-    assert lib.hcs_abi_version() == 100
+    assert lib.hcs_abi_version() == 101
     # workspace sizing needs no device for the convex solvers
     assert lib.hcs_workspace_bytes(0, 1000, 198, 79) >= 2 * 208 * 208 * 8
     # argument validation happens before any device work

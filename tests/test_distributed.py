@@ -89,3 +89,39 @@ def test_gloo_world2_reduction_matches_single_process():
     assert peak == pytest.approx(sq.max())
     summ = parallel.cube_summary(stats[0], 1.0, X * Y, 4)
     assert summ["n_failed"] == int((~ok).sum())
+
+
+def test_launcher_drives_sharded_step_world2(tmp_path):
+    """bench.py's launcher (parallel.spawn_ranks -> torch.distributed.run) and
+    its timed step (parallel.ShardedStep) at world size 2 over gloo with a fake
+    solve: the slabs partition the cube, every rank solves every configuration
+    once, and the one all-reduce yields the whole cube's statistics."""
+    import json
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from dist_step_worker import fake_truth
+
+    X, Y, n = 9, 5, 4
+    worker = Path(__file__).resolve().parent / "dist_step_worker.py"
+    rc = parallel.spawn_ranks(2, [str(worker), str(tmp_path), str(X), str(Y), str(n)],
+                              env={"OMP_NUM_THREADS": "1"})
+    assert rc == 0
+    res = [json.loads((tmp_path / f"rank{r}.json").read_text()) for r in range(2)]
+    assert [r["world"] for r in res] == [2, 2]
+    slabs = sorted(tuple(r["slab"]) for r in res)
+    assert slabs[0][0] == 0 and slabs[-1][1] == X and slabs[0][1] == slabs[1][0]
+    assert all(r["solved"] == ["gomp", "cosamp"] for r in res)
+    assert all(r["launches"] == 2 * 3 for r in res)     # (2 solver kernels + 1 SSE) x 2 configs
+    truth = [fake_truth(p) for p in range(X * Y)]
+    ok = [t[2] < 0 for t in truth]
+    expect = [float(sum(p * p for p in range(X * Y))),
+              sum(1 for t, o in zip(truth, ok) if t[1] and o),
+              sum(1 for o in ok if not o),
+              sum(1 for t, o in zip(truth, ok) if t[0] == 0 and t[1] and o),
+              sum(t[0] for t, o in zip(truth, ok) if o),
+              float(sum(range(X * Y)))]
+    for r in res:   # every rank holds the reduced statistics, identical for both configs
+        for row in r["stats"]:
+            np.testing.assert_allclose(row, expect, rtol=1e-12)

@@ -53,7 +53,8 @@ def main():
         dt = time.perf_counter() - t
         it = out.iterations.cpu().numpy()
         print(f"{args.algo} k={args.kappa} P={cube.n_pixels}: {dt * 1e3:.2f} ms, {cube.n_pixels / dt:.0f} px/s, "
-              f"iters mean {it.mean():.2f} max {it.max()} total {it.sum()}, {dt / max(it.sum(), 1) * 1e6:.2f} us/iter")
+              f"iters mean {it.mean():.2f} max {it.max()} total {it.sum()}, {dt / max(it.sum(), 1) * 1e6:.2f} us/iter"
+              + ("" if convex else f", spilled {int(out.workspace[16:24].view(torch.int64).item())}"))
         if has_ph:
             dbg(ph, 1)
             names = (["slots", "writeback", "gemm1", "epi1", "gemm2", "epi2"] if convex else
