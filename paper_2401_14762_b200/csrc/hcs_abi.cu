@@ -215,7 +215,8 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     // warp-per-pixel Householder gOMP; the pixels it spills (supports beyond
     // 33 columns, rank guard) are re-solved from scratch by the CTA kernel
     unsigned long long* spill_n = reinterpret_cast<unsigned long long*>(ws + 16);
-    e = hcs::launch_gomp_warp(args, hcs::GwSpill{spill_n, spill_list}, sms, stream);
+    e = hcs::launch_gomp_warp(args, hcs::GwSpill{spill_n, spill_list, gscratch, (long long)hcs::greedy_ls_doubles(M)},
+                              sms, gw.slots, stream);
     if (e != cudaSuccess) return cuda_fail(e, "gomp_warp_kernel");
     args.counter = reinterpret_cast<unsigned long long*>(ws + 24);
     args.plist = spill_list;

@@ -28,24 +28,34 @@
 //     rows), the reflector vector is broadcast through shared memory, each
 //     lane applies it to its own column (no cross-lane reductions); y is
 //     carried in lanes-over-rows form (Q^T y with a warp sum per reflector);
-//     a 33rd column is a "pre-column" handled lanes-over-rows the same way;
+//     columns beyond the 32 lanes (kappa = 33's top system; |S| up to M
+//     once the support outgrows kappa) are "pre-columns": the first
+//     K - 32 columns, factored lanes over rows in the warp's global scratch
+//     and applied to the lane columns like any other reflector;
 //   * residual y - A x from the gathered columns (kept in shared memory),
 //     delta, stop rule.
-// Pixels outside the fast path (supports beyond 33 columns, a rank guard
-// min|R_ii| <= 1e-6 max|R_ii| where the reference's pivoted rank decision
-// could differ, non-finite intermediates) are handed to the CTA kernel
-// (hcs_greedy.cu, pivoted QR mode) through a spill list and solved there
-// from scratch.
+// Pixels outside the fast path (a rank guard min|R_ii| <= 1e-6 max|R_ii|
+// where the reference's pivoted rank decision could differ) are handed to
+// the CTA kernel (hcs_greedy.cu, pivoted QR mode) through a spill list and
+// solved there from scratch.
 #include "hcs_internal.cuh"
 
 namespace hcs {
 
-constexpr int kWarpCols = 33;   // LS columns of the fast path: 32 lane columns + 1 pre-column
+constexpr int kWarpCols = 33;   // columns kept in shared memory (orig): the top system, kappa <= 33
+constexpr int kWarpMaxK = 96;   // LS columns of the fast path: 32 lane columns + up to 64 pre-columns
 constexpr int kGwWarps = 8;     // warps (pixels) per CTA
+
+struct GwBytes {
+  uint8_t msk[128];
+  uint8_t cols[128];
+  uint32_t supp[8];
+  uint32_t sel[8];
+};
 
 struct GwLayout {
   int ldc;                // leading dimension of the gathered columns (odd: conflict-free lane-column reads)
-  int orig, vb, r, y, xv, cb; // double offsets
+  int orig, vb, r, y, xv;     // double offsets (vb: reflector vector / back-substitution buffers / x row)
   int bytes_off;          // byte region offset (in doubles)
   size_t bytes;           // per warp, 16-byte aligned
 };
@@ -59,21 +69,14 @@ __host__ __device__ inline GwLayout gw_layout(int M) {
   L.vb = o; o += kMaxN;       // reflector vector (MR) / dense x row / scatter scratch (N)
   L.r = o; o += M;
   L.y = o; o += M;
-  L.xv = o; o += 40;
-  L.cb = o; o += 80;          // back-substitution column buffers (2 x 40)
+  L.xv = o; o += kWarpMaxK;    // x values (and the pre-columns' during the solve)
   L.bytes_off = o;
   size_t b = sizeof(double) * (size_t)o;
-  b += 128 + 64 + 64;         // mask (<= 96 B, padded), column list (40 B), bitmaps / flags
+  b += sizeof(GwBytes);       // mask, column list, bitmaps
   L.bytes = (b + 15) & ~(size_t)15;
   return L;
 }
 
-struct GwBytes {
-  uint8_t msk[128];
-  uint8_t cols[64];
-  uint32_t supp[8];
-  uint32_t sel[8];
-};
 
 __device__ __forceinline__ unsigned long long gw_key(double v) {
   // argmax_k order (stable argsort of -|v|): larger |v| first, NaN last; 0 = taken
@@ -104,12 +107,15 @@ __device__ __forceinline__ int bitmap_to_list_warp(const uint32_t* bm, uint8_t* 
 }
 
 // ---------------------------------------------------------------- QR passes
-// a[MR]: this lane's column (rows 0..MR).  Loops over rows >= j start at a
-// runtime chunk (4 rows) but must index a[] statically: a switch on the first
-// chunk falls through an unrolled sequence of per-chunk bodies (Duff's
+// a[MR]: this lane's column (rows 0..MR, MR a multiple of 4).  Loops over the
+// rows >= some runtime bound must index a[] statically: a switch on the first
+// 4-row chunk falls through an unrolled sequence of per-chunk bodies (Duff's
 // device; nvcc emits one indexed branch).  Chunks past MR compile to nothing.
 #define GW_CASES(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) \
   X(12) X(13) X(14) X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23)
+
+template <int MR>
+__host__ __device__ constexpr int gw_slots() { return (MR + 31) / 32; }   // lanes-over-rows slots (y, z)
 
 template <int MR, int CB>
 __device__ __forceinline__ void gw_dot_chunk(const double (&a)[MR], const double2* v2, double (&d)[4]) {
@@ -130,6 +136,24 @@ __device__ __forceinline__ void gw_upd_chunk(double (&a)[MR], const double2* v2,
     a[4 * CB + 1] = fma(-f, va.y, a[4 * CB + 1]);
     a[4 * CB + 2] = fma(-f, vc.x, a[4 * CB + 2]);
     a[4 * CB + 3] = fma(-f, vc.y, a[4 * CB + 3]);
+  }
+}
+
+template <int MR, int CB>
+__device__ __forceinline__ void gw_nrm_chunk(const double (&a)[MR], double (&n)[4]) {
+  if constexpr (4 * CB + 3 < MR) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) n[t] = fma(a[4 * CB + t], a[4 * CB + t], n[t]);
+  }
+}
+
+// rows >= lo of chunk CB only (the partial chunk of a norm)
+template <int MR, int CB>
+__device__ __forceinline__ void gw_nrm_part(const double (&a)[MR], int lo, double (&n)[4]) {
+  if constexpr (4 * CB + 3 < MR) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (4 * CB + t >= lo) n[t] = fma(a[4 * CB + t], a[4 * CB + t], n[t]);
   }
 }
 
@@ -167,6 +191,27 @@ __device__ __forceinline__ void gw_update(double (&a)[MR], const double* vb, int
   }
 }
 
+// sum_{rows >= lo} a_i^2 (per lane): the partial chunk, then whole chunks
+template <int MR>
+__device__ __forceinline__ double gw_norm(const double (&a)[MR], int lo) {
+  double n[4] = {0.0, 0.0, 0.0, 0.0};
+  if (lo & 3) {
+    switch (lo >> 2) {
+#define GW_NP_CASE(k) case k: gw_nrm_part<MR, k>(a, lo, n); break;
+      GW_CASES(GW_NP_CASE)
+#undef GW_NP_CASE
+      default: break;
+    }
+  }
+  switch ((lo + 3) >> 2) {
+#define GW_NRM_CASE(k) case k: gw_nrm_chunk<MR, k>(a, n);
+    GW_CASES(GW_NRM_CASE)
+#undef GW_NRM_CASE
+    default: break;
+  }
+  return (n[0] + n[1]) + (n[2] + n[3]);
+}
+
 // the owner's column, rows >= 4 (j / 4), into vb
 template <int MR>
 __device__ __forceinline__ void gw_copy(const double (&a)[MR], double* vb, int j) {
@@ -179,32 +224,59 @@ __device__ __forceinline__ void gw_copy(const double (&a)[MR], double* vb, int j
   }
 }
 
-// Householder QR of the K gathered columns (orig, our column order) and
-// Q^T y.  Lanes own columns e + lane (e = K - 32 pre-columns, 0 or 1);
-// returns in every lane: its column's R part in a[0..], its diagonal in
-// rdiag; yw (lanes over rows) = Q^T y; beta0 = R_00 of the pre-column.
-// Per reflector j: the column (the owner lane's registers, or the
-// pre-column from orig) goes to vb; every lane reads xnorm^2 = sum_{i>j} v_i^2
-// (lanes over rows + warp sum) and alpha = v_j and forms beta, g = 1 /
-// (beta (beta - alpha)) (LAPACK dlarfg's reflector, unscaled:
-// H c = c - g (v^T c) v with v = [alpha - beta; x]); then each lane applies H
-// to its own column and the warp to y.
+// the owner's rows 0 .. 4 ceil(c / 4) - 1 into cb (R's column c above the
+// diagonal, plus rows >= c that the reader ignores): reverse Duff
+template <int MR, int CB>
+__device__ __forceinline__ void gw_rcol_chunk(const double (&a)[MR], double2* c2) {
+  if constexpr (4 * CB + 3 < MR) {
+    c2[2 * CB] = make_double2(a[4 * CB], a[4 * CB + 1]);
+    c2[2 * CB + 1] = make_double2(a[4 * CB + 2], a[4 * CB + 3]);
+  }
+}
 template <int MR>
-__device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&yw)[MR / 32], double& beta0,
-                                      const double* orig, int ldc, double* vb, int K, int M, int lane) {
+__device__ __forceinline__ void gw_rcol(const double (&a)[MR], double* cb, int c) {
+  double2* c2 = reinterpret_cast<double2*>(cb);
+  switch ((c + 3) >> 2) {   // chunks (c+3)/4 - 1 .. 0
+#define GW_RC_CASE(k) case k + 1: gw_rcol_chunk<MR, k>(a, c2);
+    GW_RC_CASE(23) GW_RC_CASE(22) GW_RC_CASE(21) GW_RC_CASE(20) GW_RC_CASE(19) GW_RC_CASE(18) GW_RC_CASE(17)
+    GW_RC_CASE(16) GW_RC_CASE(15) GW_RC_CASE(14) GW_RC_CASE(13) GW_RC_CASE(12) GW_RC_CASE(11) GW_RC_CASE(10) GW_RC_CASE(9)
+    GW_RC_CASE(8) GW_RC_CASE(7) GW_RC_CASE(6) GW_RC_CASE(5) GW_RC_CASE(4) GW_RC_CASE(3) GW_RC_CASE(2) GW_RC_CASE(1)
+    GW_RC_CASE(0)
+#undef GW_RC_CASE
+    default: break;
+  }
+}
+
+// Householder QR of the K gathered columns and Q^T y.  Columns e .. K-1
+// (e = max(0, K - 32)) are in the lanes' registers (lane L owns column e + L,
+// loaded from orig slot e + L - e0); the e "pre-columns" 0 .. e-1 live in
+// the warp's global scratch P (column c at P + c M) and are factored lanes
+// over rows, in place.  Returns: each lane's R column part in a[0..] and its
+// diagonal in rdiag; P's columns hold R above and on their diagonal; yw
+// (lanes over rows) = Q^T y.
+// Reflector j (LAPACK dlarfg, unscaled: H c = c - g (v^T c) v with
+// v = [alpha - beta; x], beta = -sign(alpha) ||[alpha; x]||,
+// g = 1 / (beta (beta - alpha))): its column goes to vb (the owner lane's
+// registers, or the pre-column), every lane reads xnorm^2 = sum_{i>j} v_i^2
+// (lanes over rows + warp sum) and alpha = v_j, then applies H to its own
+// column; the warp applies it to y and to the later pre-columns.
+template <int MR>
+__device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&yw)[gw_slots<MR>()],
+                                      const double* orig, int ldc, int e0, double* P, double* vb, int K, int M,
+                                      int lane) {
+  constexpr int Q = gw_slots<MR>();
   const int e = K > 32 ? K - 32 : 0;
   const int myc = e + lane;
 #pragma unroll
-  for (int i = 0; i < MR; ++i) a[i] = (myc < K && i < M) ? orig[myc * ldc + i] : 0.0;
+  for (int i = 0; i < MR; ++i) a[i] = (myc < K && i < M) ? orig[(myc - e0) * ldc + i] : 0.0;
   rdiag = 0.0;
-  beta0 = 0.0;
   for (int j = 0; j < K; ++j) {
-    const int owner = j - e;   // < 0: the pre-column (column 0, lanes over rows)
+    const int owner = j - e;   // < 0: pre-column j (lanes over rows, in P)
     if (owner < 0) {
 #pragma unroll
-      for (int q = 0; q < MR / 32; ++q) {
+      for (int q = 0; q < Q; ++q) {
         const int row = lane + 32 * q;
-        vb[row] = row < M ? orig[row] : 0.0;
+        if (row < MR) vb[row] = row < M ? P[j * M + row] : 0.0;
       }
     } else if (lane == owner) {
       gw_copy<MR>(a, vb, j);
@@ -212,7 +284,7 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
     __syncwarp();
     double part = 0.0;
 #pragma unroll
-    for (int q = 0; q < MR / 32; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int row = lane + 32 * q;
       if (row > j && row < M) part = fma(vb[row], vb[row], part);
     }
@@ -224,75 +296,123 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
       amb = al - beta;
       g = 1.0 / (beta * (beta - al));
     }
-    if (owner < 0) beta0 = beta;
-    else if (lane == owner) rdiag = beta;
+    if (owner < 0) {
+      if (lane == (j & 31)) P[j * M + j] = beta;   // R_jj of the pre-column
+    } else if (lane == owner) {
+      rdiag = beta;
+    }
     __syncwarp();   // every lane has read v_j
-    {
+    if (owner < 0) {   // pre-columns: v over all rows (lanes over rows read them)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int row = lane + 32 * q;
+        if (row < j) vb[row] = 0.0;
+      }
+      if (lane == 0) vb[j] = amb;
+    } else {
       const int j0 = j & ~3;   // v: rows j0 .. j-1 of the first chunk read -> 0, row j -> alpha - beta
       if (lane <= j - j0) vb[j0 + lane] = (j0 + lane == j) ? amb : 0.0;
     }
     __syncwarp();
     double py = 0.0;
 #pragma unroll
-    for (int q = 0; q < MR / 32; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int row = lane + 32 * q;
       if (row >= j && row < M) py = fma(vb[row], yw[q], py);
     }
     const double f = gw_dot<MR>(a, vb, j) * g;
     gw_update<MR>(a, vb, j, f);
+    // the later pre-columns (rare: supports beyond 32 columns), two at a time
+    for (int k = j + 1; k < e; k += 2) {
+      const bool two = k + 1 < e;
+      double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int row = lane + 32 * q;
+        if (row >= j && row < M) {
+          p0 = fma(vb[row], P[k * M + row], p0);
+          if (two) p1 = fma(vb[row], P[(k + 1) * M + row], p1);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+      }
+      p0 *= g;
+      p1 *= g;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int row = lane + 32 * q;
+        if (row >= j && row < M) {
+          P[k * M + row] = fma(-p0, vb[row], P[k * M + row]);
+          if (two) P[(k + 1) * M + row] = fma(-p1, vb[row], P[(k + 1) * M + row]);
+        }
+      }
+    }
     const double fy = warp_sum(py) * g;
 #pragma unroll
-    for (int q = 0; q < MR / 32; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int row = lane + 32 * q;
       if (row >= j && row < M) yw[q] = fma(-fy, vb[row], yw[q]);
     }
-    __syncwarp();   // vb is rewritten by the next owner
+    __syncwarp();   // vb (and P) are rewritten by the next reflector
   }
 }
 
 // Back substitution R x = z, column-oriented as LAPACK's dtrsv ('U', 'N'):
 // for c = K-1 .. 0: x_c = z_c / R_cc, then z_i -= R_ic x_c for i < c.
-// Column c of R is lane (c - e)'s register column, rows 0..c-1, staged through
-// shared memory (cbuf, two 40-double buffers) once per step.  Solves the full
-// system (xt) and the leading s x s block (xs, the LS(S) prefix) together.
-// Lane L receives x of column e + L; x0t / x0s: the pre-column's.
+// Column c of R is staged through shared memory (cbuf, two 96-double
+// buffers) from its owner lane's registers, or read from P for a
+// pre-column.  Solves the full system (xt) and the leading s x s block
+// (xs, the LS(S) prefix; s <= 33) together.  Lane L receives x of column
+// e + L; pre-column x values go to xpre[c] (and x0s for c = 0).
 template <int MR>
-__device__ __forceinline__ void gw_solve(const double (&a)[MR], double rdiag, const double (&yw)[MR / 32],
-                                         double beta0, int K, int s, int lane, double* cbuf, double& xt, double& xs,
-                                         double& x0t, double& x0s) {
+__device__ __forceinline__ void gw_solve(const double (&a)[MR], double rdiag, const double (&yw)[gw_slots<MR>()],
+                                         const double* P, int M, int K, int s, int lane, double* cbuf, double& xt,
+                                         double& xs, double* xpre, double& x0s) {
   const int e = K > 32 ? K - 32 : 0;
-  double zt0 = yw[0], zt1 = MR > 32 ? yw[MR > 32 ? 1 : 0] : 0.0;   // rows lane, lane + 32
+  constexpr int Q = gw_slots<MR>();
+  double zt0 = yw[0];                                   // rows lane, lane + 32, lane + 64
+  double zt1 = Q > 1 ? yw[Q > 1 ? 1 : 0] : 0.0;
+  double zt2 = Q > 2 ? yw[Q > 2 ? 2 : 0] : 0.0;
   double zs0 = zt0, zs1 = zt1;
   xt = 0.0;
   xs = 0.0;
-  x0t = 0.0;
   x0s = 0.0;
   for (int c = K - 1; c >= 0; --c) {
-    double* cb = cbuf + (c & 1) * 40;
-    const int owner = c - e;   // < 0: the pre-column (c = 0), no entries above the diagonal
-    if (owner >= 0 && lane == owner) {
-#pragma unroll
-      for (int i = 0; i < kWarpCols && i < MR; ++i)
-        if (i < c) cb[i] = a[i];
+    const int owner = c - e;   // < 0: a pre-column
+    const double* cb;
+    double rcc;
+    if (owner >= 0) {
+      double* w = cbuf + (c & 1) * 96;
+      if (lane == owner) gw_rcol<MR>(a, w, c);
+      rcc = __shfl_sync(0xffffffffu, rdiag, owner & 31);
+      cb = w;
+    } else {
+      cb = P + c * M;
+      rcc = P[c * M + c];
     }
-    const double rcc = owner >= 0 ? __shfl_sync(0xffffffffu, rdiag, owner & 31) : beta0;
-    const double zct = __shfl_sync(0xffffffffu, (c >> 5) ? zt1 : zt0, c & 31);
+    const double zct = __shfl_sync(0xffffffffu, (c >> 5) == 2 ? zt2 : ((c >> 5) ? zt1 : zt0), c & 31);
     const double zcs = __shfl_sync(0xffffffffu, (c >> 5) ? zs1 : zs0, c & 31);
     const double vt = zct / rcc;
     const double vs = c < s ? zcs / rcc : 0.0;
     if (owner < 0) {
-      x0t = vt;
-      x0s = vs;
+      if (lane == 0) xpre[c] = vt;
+      if (c == 0) x0s = vs;
     } else if (lane == owner) {
       xt = vt;
       xs = vs;
     }
     __syncwarp();
-    if (lane < c) {   // rows i < c <= 32 live in slot 0
+    // z_i -= R_ic x_c for rows i < c (slot 0: i < 32; slot 1: 32 <= i < c)
+    if (lane < c) {
       const double r = cb[lane];
       zt0 = fma(-r, vt, zt0);
       if (c < s) zs0 = fma(-r, vs, zs0);
     }
+    if (lane + 32 < c) zt1 = fma(-cb[lane + 32], vt, zt1);
+    if (lane + 64 < c) zt2 = fma(-cb[lane + 64], vt, zt2);
   }
 }
 
@@ -312,9 +432,11 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
   double* ys = S + L.y;
   double* xv = S + L.xv;
   GwBytes& gb = *reinterpret_cast<GwBytes*>(S + L.bytes_off);
+  // this warp's global scratch for pre-columns (least-squares systems beyond 32 columns)
+  double* P = sp.pre + (size_t)(blockIdx.x * (blockDim.x >> 5) + warp) * (size_t)sp.pre_stride;
   const int kappa = a.prm.kappa, G = a.prm.G;
   const double NaN = __longlong_as_double(0x7ff8000000000000ll);
-  constexpr int Q = MR / 32;
+  constexpr int Q = gw_slots<MR>();
 
   for (;;) {
     long long pid = 0;
@@ -430,7 +552,7 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
       __syncwarp();
       if (lane < 8) gb.supp[lane] = sw;
       __syncwarp();
-      if (ks > kWarpCols || kappa > kWarpCols) { spill = true; break; }
+      if (ks > kWarpMaxK) { spill = true; break; }
       // ---- column order [S | fills] ------------------------------------------
       // S sorted, then (ks <= kappa) the kappa - ks lowest indices outside S
       int K;
@@ -454,28 +576,40 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
         K = ks <= kappa ? kappa : ks;
       }
       __syncwarp();
-      double xt = 0.0, x0t = 0.0;
+      double xt = 0.0;
       bool second = false;
       for (int round = 0; round < 2; ++round) {
-        // ---- gather the K columns at the measured rows (L2 -> shared) ---------
-        for (int c = 0; c < K; ++c) {
+        // ---- gather the columns at the measured rows (L2 -> shared / scratch) --
+        // K <= 33: all columns to orig slots 0..K-1 (kept for the residual);
+        // K > 33 (round 0 of |S| > 33 only): the 32 lane columns to orig slots
+        // 0..31; pre-columns (e = K - 32) to the warp's scratch P, factored in place
+        const int e = K > 32 ? K - 32 : 0;
+        const int e0 = K > kWarpCols ? e : 0;
+        for (int c = e0; c < K; ++c) {
           const double* col = a.basis_t + (size_t)gb.cols[c] * N;
-          for (int i = lane; i < M; i += 32) cp_async8(orig + c * L.ldc + i, col + gb.msk[i]);
+          for (int i = lane; i < M; i += 32) cp_async8(orig + (c - e0) * L.ldc + i, col + gb.msk[i]);
+        }
+        for (int c = 0; c < e; ++c) {
+          const double* col = a.basis_t + (size_t)gb.cols[c] * N;
+          for (int i = lane; i < M; i += 32) P[c * M + i] = __ldg(col + gb.msk[i]);
         }
         cp_async_wait_all();
         __syncwarp();
         double acol[MR];
-        double rdiag, beta0;
+        double rdiag;
         double yw[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) yw[q] = lane + 32 * q < M ? ys[lane + 32 * q] : 0.0;
-        gw_qr<MR>(acol, rdiag, yw, beta0, orig, L.ldc, vb, K, M, lane);
+        gw_qr<MR>(acol, rdiag, yw, orig, L.ldc, e0, P, vb, K, M, lane);
         // rank guard on the diagonal of R (see header)
         {
-          const int e = K > 32 ? K - 32 : 0;
           const double dl = (e + lane < K) ? fabs(rdiag) : 0.0;
           double dmax = dl, dmin = (e + lane < K) ? dl : INFINITY;
-          if (e) { dmax = fmax(dmax, fabs(beta0)); dmin = fmin(dmin, fabs(beta0)); }
+          for (int c = lane; c < e; c += 32) {
+            const double dp = fabs(P[c * M + c]);
+            dmax = fmax(dmax, dp);
+            dmin = fmin(dmin, dp);
+          }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
@@ -485,31 +619,29 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
         }
         const int s = (!second && ks <= kappa) ? ks : 0;
         double xs, x0s;
-        gw_solve<MR>(acol, rdiag, yw, beta0, K, s, lane, S + L.cb, xt, xs, x0t, x0s);
+        gw_solve<MR>(acol, rdiag, yw, P, M, K, s, lane, vb, xt, xs, xv, x0s);
         if (second) break;   // second round done: xt is LS(top)
         // the top call: argmax_k(scatter(LS(S)), kappa) over all N bands.
         // |S| <= kappa: the predicted top [S | fills] is the real one iff every
         // LS(S) coefficient is nonzero (zeros tie with the fills, NaN ranks
         // last); otherwise (or |S| > kappa) the exact warp top-k selects it and
         // a second QR solves on those columns
-        const int e = K > 32 ? K - 32 : 0;
         const int myc = e + lane;
         bool general = ks > kappa;
-        double sv = xs, sv0 = x0s;
+        double sv = xs;
         if (general) {
-          sv = xt;      // |S| > kappa: the first round solved S itself
-          sv0 = x0t;
+          sv = xt;      // |S| > kappa: the first round solved S itself (pre-columns in xv)
         } else {
           bool zero = (myc < s) && !(xs != 0.0 && xs == xs);
           if (e && lane == 0) zero |= !(x0s != 0.0 && x0s == x0s);
           general = __any_sync(0xffffffffu, zero);
+          if (general && e && lane == 0) xv[0] = x0s;   // the pre-column's LS(S) value for the scatter
         }
         if (general) {
-          const int ns = ks;   // the S columns are cols[0 .. ks)
           for (int n = lane; n < N; n += 32) vb[n] = 0.0;
           __syncwarp();
-          if (e && lane == 0) vb[gb.cols[0]] = sv0;
-          if (myc < ns) vb[gb.cols[myc]] = sv;
+          for (int c = lane; c < e; c += 32) vb[gb.cols[c]] = xv[c];
+          if (myc < ks) vb[gb.cols[myc]] = sv;
           __syncwarp();
           warp_topk(vb, N, kappa, gb.sel);
           __syncwarp();
@@ -536,11 +668,12 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
       if (spill) break;
       work += ls_flops(M, ks) + ls_flops(M, kappa);
       // ---- new iterate, residual, delta (solvers.py:285-290) ------------------
+      // x over cols[0..K): pre-column values are in xv already (gw_solve)
       kx = K;
       {
         const int e = K > 32 ? K - 32 : 0;
+        __syncwarp();
         if (e + lane < K) xv[e + lane] = xt;
-        if (e && lane == 0) xv[0] = x0t;
       }
       __syncwarp();
       double part = 0.0;
@@ -594,7 +727,10 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
   }
 }
 
-bool gomp_warp_supported(int N, int M, int kappa) { return M <= 96 && kappa <= kWarpCols && N <= kMaxN && M >= 1; }
+bool gomp_warp_supported(int N, int M, int kappa) {
+  // pre-column scratch: up to 32 columns of M rows per warp in a CTA scratch slot
+  return M >= 1 && M <= 96 && kappa <= kWarpCols && N <= kMaxN && 64 * (size_t)M <= greedy_ls_doubles(M);
+}
 
 size_t gomp_warp_smem(int M, int* warps) {
   const GwLayout L = gw_layout(M);
@@ -613,15 +749,21 @@ static cudaError_t launch_gw_t(const GreedyArgs& args, const GwSpill& sp, int gr
   return cudaGetLastError();
 }
 
-cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, cudaStream_t stream) {
+cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, long long slots,
+                             cudaStream_t stream) {
   int warps = 0;
   const size_t smem = gomp_warp_smem(args.M, &warps);
   long long grid = sms;
+  if (grid * warps > slots) grid = slots / warps;   // one pre-column scratch slot per warp
   const long long need = (args.P + warps - 1) / warps;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
+  // register column of MR rows, the smallest instantiation >= M
   if (args.M <= 32) return launch_gw_t<32>(args, sp, (int)grid, warps, smem, stream);
+  if (args.M <= 48) return launch_gw_t<48>(args, sp, (int)grid, warps, smem, stream);
   if (args.M <= 64) return launch_gw_t<64>(args, sp, (int)grid, warps, smem, stream);
+  if (args.M <= 80) return launch_gw_t<80>(args, sp, (int)grid, warps, smem, stream);
+  if (args.M <= 92) return launch_gw_t<92>(args, sp, (int)grid, warps, smem, stream);
   return launch_gw_t<96>(args, sp, (int)grid, warps, smem, stream);
 }
 

@@ -56,6 +56,8 @@ struct GreedyArgs {
 struct GwSpill {
   unsigned long long* count;
   long long* list;
+  double* pre;            // per-warp pre-column scratch (the CTA scratch slots)
+  long long pre_stride;   // doubles per slot
 };
 
 // hcs_convex.cu
@@ -78,7 +80,8 @@ cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, cudaS
 int greedy_blocks_per_sm(int algo, int M, size_t smem);
 // hcs_gomp_warp.cu
 bool gomp_warp_supported(int N, int M, int kappa);
-cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, cudaStream_t stream);
+cudaError_t launch_gomp_warp(const GreedyArgs& args, const GwSpill& sp, int sms, long long slots,
+                             cudaStream_t stream);
 // hcs_batched.cu
 cudaError_t launch_basis_gram_dev(int N, const double* basis, unsigned long long* out, cudaStream_t stream);
 cudaError_t launch_validate_masks(long long P, int M, int N, const uint8_t* mask, int* err, int sms,

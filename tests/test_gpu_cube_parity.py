@@ -7,10 +7,20 @@ iterations or flags are classified with selection traces from both sides: each
 must be a roundoff-degenerate tie on the oracle side AND be reproduced by the
 forced-selection replay; anything else is a real mismatch and fails the test.
 The cube PSNR over the agreeing pixels must match to 0.01 dB, and for solvers
-without tie exceptions the whole-cube PSNR must too.  (For gOMP the tie
-pixels carry a large share of the squared error, so its whole-cube PSNR is
-not roundoff-stable even for the oracle itself: tools/cube_parity.py --perturb,
-profiles/cube_parity_r01.jsonl.)
+without tie exceptions the whole-cube PSNR must too.
+
+gOMP's whole-cube PSNR is not roundoff-stable even for the oracle itself: its
+second pass selects atoms from A^T r with r at roundoff level, and the tie
+pixels carry most of the squared error.  For gOMP the whole cube is therefore
+judged against the oracle's own roundoff band: an ensemble of oracle re-solves
+of y (1 + 2^-52 N(0,1)) (tools/cube_parity.py --ensemble,
+profiles/gomp_ls_statistics_r02.txt).  The GPU must not disagree with the
+oracle on more pixels than 1.3 x the ensemble's largest flip count (the
+round-1 normal-equations solver failed this at 2.5x: a systematic bias, not
+roundoff), and its cube dPSNR must lie inside the ensemble's range (with the
+oracle itself, dPSNR 0) widened by 25% of its width on each side -- with n
+exchangeable draws a further draw falls outside their range with probability
+2 / (n + 1), which the widening absorbs.
 """
 
 import math
@@ -30,6 +40,8 @@ from parity import compare  # noqa: E402
 from test_gpu_parity import decode_trace, make_replay  # noqa: E402
 
 pytestmark = pytest.mark.gpu
+
+ENSEMBLE = 6
 
 CASES = [
     ("jasper", "gomp", dict(kappa=24, atoms_per_iter=4), None, 0.02),       # cfg1
@@ -105,5 +117,21 @@ def test_full_cube_parity(pool, cubes, cube_name, algo, params, cap, max_tie_fra
     assert abs(pg - pr) <= 0.01 or (pg > 200 and pr > 200), (pg, pr)
     if not len(idx):
         assert abs(_db(sse_g.sum(), peak, c.spectra.size) - _db(sse_r.sum(), peak, c.spectra.size)) <= 0.01
+    if algo == "gomp":
+        p_ref = _db(sse_r.sum(), peak, c.spectra.size)
+        dps, flips = [0.0], []
+        for e in range(ENSEMBLE):
+            rng = np.random.default_rng(100 + e)
+            yp = c.y * (1.0 + 2.0 ** -52 * rng.standard_normal(c.y.shape))
+            rp = oc.solve_cube(algo, c.basis, yp, c.masks, ocfg, pool=ex, chunk=256)
+            d_p = c.spectra - rp.x @ c.basis.T
+            dps.append(_db(float(np.einsum("pn,pn->", d_p, d_p)), peak, c.spectra.size) - p_ref)
+            flips.append(int((rp.iterations != ref.iterations).sum()))
+        dp_gpu = _db(sse_g.sum(), peak, c.spectra.size) - p_ref
+        lo, hi = min(dps), max(dps)
+        print(f"  gOMP band: GPU dPSNR {dp_gpu:+.2f} dB, {len(idx)} disagreeing; oracle ensemble dPSNR "
+              f"[{lo:+.2f}, {hi:+.2f}] dB, flips {flips}")
+        assert len(idx) <= 1.3 * max(flips), (len(idx), flips)
+        assert lo - 0.25 * (hi - lo) <= dp_gpu <= hi + 0.25 * (hi - lo), (dp_gpu, dps)
     print(f"{cube_name} {algo} {params}: {c.n_pixels} px, {len(idx)} replay-confirmed tie exceptions, "
           f"agreeing-pixel PSNR {pg:.4f} / {pr:.4f} dB")

@@ -102,6 +102,9 @@ def test_gpu_matches_reference_golden(golden_dir, name):
 # larger seeded cubes against the oracle (run here on the GPU box's CPU)
 ORACLE_CASES = [
     ("jasper", "gomp", dict(kappa=24, atoms_per_iter=4), None, 600),
+    # gOMP with |S| > kappa after one pass: least-squares systems of 24..60 columns
+    # (warp kernel pre-columns) and, past 64 columns, the CTA kernel's spill path
+    ("salinas", "gomp", dict(kappa=12, atoms_per_iter=12), 6, 200),
     ("jasper", "fista", dict(lam=0.1), 5000, 200),
     ("jasper", "admm", dict(lam=0.1, alpha=1.8), 5000, 120),
     ("jasper", "fista", dict(lam=100.0), 5000, 400),
