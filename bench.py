@@ -74,18 +74,26 @@ def host_cores():
 CPU_STRIDE = 97
 
 
+# pixels of the strided sample timed per configuration and step (about 1 s of
+# work each on 16 host cores at --ref-budget 1; "all" = the whole sample)
+CPU_SAMPLE_PX = {"fista_l0.1": 8192, "admm_l0.1": 1536, "admm_l100": 6144, "cosamp_k27": 6144}
+
+
 class CpuBaseline:
     """The reference's algorithm on the host cores (the oracle port, one
     worker process per core, OpenBLAS single-threaded per worker, as
     SURVEY.md §8(d) / BASELINE.md §2 prescribe), timed on a fixed
     deterministic sample of the workload cube: every 97th pixel by global
     x-major index (18,327 of the scaling cube's 1,777,664, spread over all 16
-    tiles).  Each step solves, for every solver configuration, the next
-    round-robin chunk of that sample sized to ~``budget`` seconds of work;
-    a configuration's rate is chunk pixels / wall time of its pool map, the
-    step's value their harmonic aggregate (10 configs x P / sum of times, the
-    way `value` aggregates).  Also reports the sum of per-pixel solve times
-    (the reference's recovery_time_s semantics, solvers.py:510)."""
+    tiles).  Each configuration times a FIXED, evenly spaced subset of that
+    sample (CPU_SAMPLE_PX x --ref-budget pixels, else the whole sample), the
+    same subset in every step and in both the reference arm and the
+    cpu_baseline leg, so the two measure the same work (per-pixel cost is
+    heavy-tailed: CoSaMP pixels that cycle to the 2000-iteration cap cost 1000x
+    a converging one).  A configuration's rate = subset pixels / wall time of
+    its pool map; a step's value = the harmonic aggregate over configurations
+    (the way `value` aggregates); also the sum of per-pixel solve times (the
+    reference's recovery_time_s semantics, solvers.py:510)."""
 
     def __init__(self, workload, budget, cores, stride=CPU_STRIDE):
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
@@ -99,25 +107,28 @@ class CpuBaseline:
         self.stride, self.budget, self.cores = stride, budget, cores
         self.pool = ProcessPoolExecutor(max_workers=cores, initializer=oc.single_thread_blas)
         list(self.pool.map(abs, range(4 * cores)))        # start the workers outside the timing
-        self.offset = {label(a, p): 0 for a, p, _ in self.solvers}
-        self.size = {label(a, p): 4 * cores for a, p, _ in self.solvers}
+        S = self.sample.n_pixels
+        self.subset = {}
+        for algo, params, _ in self.solvers:
+            lab = label(algo, params)
+            n = min(S, max(1, int(CPU_SAMPLE_PX.get(lab, S) * budget)))
+            self.subset[lab] = (np.arange(n) * S) // n
 
     def step(self):
-        S = self.sample.n_pixels
         rates, sizes, sum_el = {}, {}, {}
         for algo, params, cap in self.solvers:
             lab = label(algo, params)
             cfg = self.oc.OracleConfig(max_iter=cap or 0, **params)
-            n = min(self.size[lab], S)
-            idx = (self.offset[lab] + np.arange(n)) % S
+            idx = self.subset[lab]
+            n = len(idx)
             y, masks = np.ascontiguousarray(self.sample.y[idx]), np.ascontiguousarray(self.sample.masks[idx])
             t0 = time.perf_counter()
-            res = self.oc.solve_cube(algo, self.sample.basis, y, masks, cfg, chunk=max(1, n // (4 * self.cores)),
-                                     pool=self.pool)
+            # 8 tasks per worker: balances the heavy-tailed configurations without
+            # letting the per-task pickling of the basis dominate the cheap ones
+            res = self.oc.solve_cube(algo, self.sample.basis, y, masks, cfg,
+                                     chunk=max(1, n // (8 * self.cores)), pool=self.pool)
             dt = time.perf_counter() - t0
             rates[lab], sizes[lab], sum_el[lab] = n / dt, n, float(res.elapsed.sum())
-            self.offset[lab] = (self.offset[lab] + n) % S
-            self.size[lab] = int(min(S, max(4 * self.cores, n * self.budget / max(dt, 1e-3))))
         agg = len(rates) / sum(1.0 / r for r in rates.values())
         return agg, rates, sizes, sum_el
 
@@ -136,7 +147,8 @@ class CpuBaseline:
             "value": value, "unit": "spectra/s", "cores": self.cores, "kind": "port",
             "sample": (f"every {self.stride}th pixel of the {'x'.join(map(str, self.shape))} workload cube "
                        f"(global x-major index p % {self.stride} == 0: {self.sample.n_pixels} px over all tiles); "
-                       f"per step and solver config the next round-robin chunk of ~{self.budget:g}s of work; "
+                       f"per solver config a fixed evenly spaced subset of it, the same in every step "
+                       f"({ {k: len(v) for k, v in self.subset.items()} } px); "
                        f"{steps} timed steps after {warmup} warm-up"),
             "per_solver": per, "pixels_timed": px,
             "sum_elapsed_s": sel,
@@ -490,7 +502,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--ref-budget", type=float, default=1.0,
-                    help="seconds of CPU work per solver config per step (reference arm and the cpu_baseline leg)")
+                    help="scale of the CPU sample per solver config (1: ~1 s of work per config and step on 16 "
+                         "cores; reference arm and the cpu_baseline leg)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--only", default="", help="comma-separated solver labels (diagnostics)")

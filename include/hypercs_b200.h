@@ -104,6 +104,11 @@ typedef struct {
 /* Version of the ABI (major * 100 + minor). */
 int hcs_abi_version(void);
 
+/* 1 for a bounds-checked build (-DHCS_CHECKS: shared-memory poison and
+ * canaries, device index assertions; hcs_recover_status then reports a
+ * failed check as HCS_ECUDA), else 0. */
+int hcs_checked_build(void);
+
 /* Human-readable message for the last error on this host thread. */
 const char* hcs_last_error(void);
 

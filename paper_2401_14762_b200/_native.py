@@ -20,7 +20,7 @@ EXPORTS = (
     "hcs_abi_version", "hcs_last_error", "hcs_workspace_bytes", "hcs_recover", "hcs_recover_status",
     "hcs_soft_threshold", "hcs_argmax_k", "hcs_least_squares", "hcs_residual_delta", "hcs_lipschitz",
     "hcs_psnr_partials", "hcs_dmma_peak_tflops", "hcs_synth_spectra", "hcs_sparsify_measure",
-    "hcs_sse_coeff_partials", "hcs_recover_launches", "hcs_check_basis",
+    "hcs_sse_coeff_partials", "hcs_recover_launches", "hcs_check_basis", "hcs_checked_build",
 )
 
 

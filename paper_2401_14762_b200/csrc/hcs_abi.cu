@@ -69,6 +69,14 @@ extern "C" {
 
 int hcs_abi_version(void) { return 101; }
 
+int hcs_checked_build(void) {
+#ifdef HCS_CHECKS
+  return 1;
+#else
+  return 0;
+#endif
+}
+
 const char* hcs_last_error(void) { return g_err.c_str(); }
 
 size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
@@ -201,6 +209,10 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   e = hcs::launch_transpose_basis(basis, N, basis_t, stream);
   if (e != cudaSuccess) return cuda_fail(e, "transpose_basis_kernel");
   hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch, basis_t};
+  args.slots = gw.slots;
+#ifdef HCS_CHECKS
+  if (const char* ov = getenv("HCS_CHECK_SELFTEST")) args.selftest = atoi(ov);
+#endif
   // gOMP solves by Householder QR (the reference's algorithm): its
   // iteration-2 selections are made on roundoff-level residuals, and CSNE's
   // more accurate solutions shift which noise columns win (2.5x the oracle's
@@ -264,6 +276,12 @@ int hcs_recover_status(const void* workspace, void* stream_) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return cuda_fail(e, "status");
   if (flag & hcs::kErrMask) return fail(HCS_EINVAL, "mask entries must be strictly increasing band indices < N");
+  if (flag & hcs::kErrCheck) {   // bounds-checked builds only
+    int line = 0;
+    cudaMemcpy(&line, static_cast<const unsigned char*>(workspace) + 48, sizeof(int), cudaMemcpyDeviceToHost);
+    return fail(HCS_ECUDA, "device bounds check failed (source line " + std::to_string(line) +
+                               "; 1 = shared-memory canary)");
+  }
   if (flag) return fail(HCS_ENONFINITE, "array must not contain infs or NaNs");
   return HCS_OK;
 }

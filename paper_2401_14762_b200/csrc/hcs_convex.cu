@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   constexpr int MAXRB = (SL == 32) ? 2 : 4;   // row blocks per warp
   constexpr int NV = 2 * CB;                  // per-lane column partials
   extern __shared__ __align__(16) unsigned char smraw[];
+  hcs_smem_poison(smraw, a.smem_bytes);
   const int Np = a.Np, M = a.M, N = a.N, KS = Np >> 2;
   const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int rb0, nrb;
@@ -553,6 +554,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   if (threadIdx.x == 0)
     for (int k = 0; k < 15; ++k) atomicAdd(&g_phase_cx[k], (unsigned long long)cph[k]);
 #endif
+  hcs_smem_canary(smraw, a.smem_bytes, a.err);
 }
 
 // Fragment-order copies of Psi and Psi^T (layout of tile_gemm), and
@@ -784,10 +786,12 @@ int convex_ctas_per_sm(int algo, int Np, int M, int slots) {
 template <int ALGO, int SL, int MAXT, int MINB>
 static cudaError_t launch_convex_t(const ConvexArgs& args, int grid, size_t smem, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, SL, MAXT, MINB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + kSmemExtra));
   if (e != cudaSuccess) return e;
   const int warps = SL == 32 ? engine_warps(args.Np) : engine_warps16(args.Np);
-  convex_kernel<ALGO, SL, MAXT, MINB><<<grid, 32 * warps, smem, stream>>>(args);
+  ConvexArgs ca = args;
+  ca.smem_bytes = (unsigned)smem;
+  convex_kernel<ALGO, SL, MAXT, MINB><<<grid, 32 * warps, smem + kSmemExtra, stream>>>(ca);
   return cudaGetLastError();
 }
 

@@ -118,13 +118,14 @@ template <int MR>
 __host__ __device__ constexpr int gw_slots() { return (MR + 31) / 32; }   // lanes-over-rows slots (y, z)
 
 template <int MR, int CB>
-__device__ __forceinline__ void gw_dot_chunk(const double (&a)[MR], const double2* v2, double (&d)[4]) {
+__device__ __forceinline__ void gw_dot_chunk(const double (&a)[MR], const double2* v2, double (&d)[8]) {
   if constexpr (4 * CB + 3 < MR) {
+    constexpr int o = 4 * (CB & 1);   // even / odd chunks: two sets of four partial sums (FP64 latency)
     const double2 va = v2[2 * CB], vc = v2[2 * CB + 1];
-    d[0] = fma(va.x, a[4 * CB], d[0]);
-    d[1] = fma(va.y, a[4 * CB + 1], d[1]);
-    d[2] = fma(vc.x, a[4 * CB + 2], d[2]);
-    d[3] = fma(vc.y, a[4 * CB + 3], d[3]);
+    d[o] = fma(va.x, a[4 * CB], d[o]);
+    d[o + 1] = fma(va.y, a[4 * CB + 1], d[o + 1]);
+    d[o + 2] = fma(vc.x, a[4 * CB + 2], d[o + 2]);
+    d[o + 3] = fma(vc.y, a[4 * CB + 3], d[o + 3]);
   }
 }
 
@@ -168,7 +169,7 @@ __device__ __forceinline__ void gw_copy_chunk(const double (&a)[MR], double2* v2
 // d = sum_{rows >= 4 (j / 4)} v_i a_i  (v is zero on the rows below j)
 template <int MR>
 __device__ __forceinline__ double gw_dot(const double (&a)[MR], const double* vb, int j) {
-  double d[4] = {0.0, 0.0, 0.0, 0.0};
+  double d[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double2* v2 = reinterpret_cast<const double2*>(vb);
   switch (j >> 2) {
 #define GW_DOT_CASE(k) case k: gw_dot_chunk<MR, k>(a, v2, d);
@@ -176,7 +177,7 @@ __device__ __forceinline__ double gw_dot(const double (&a)[MR], const double* vb
 #undef GW_DOT_CASE
     default: break;
   }
-  return (d[0] + d[1]) + (d[2] + d[3]);
+  return ((d[0] + d[4]) + (d[1] + d[5])) + ((d[2] + d[6]) + (d[3] + d[7]));
 }
 
 // a_i -= f v_i on the rows >= 4 (j / 4)
@@ -360,6 +361,13 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
   }
 }
 
+// z / r given ri ~ 1/r: q = z ri, corrected by the exact residual z - q r
+// (one FMA-based correction: the quotient within an ulp of z / r)
+__device__ __forceinline__ double gw_div(double z, double r, double ri) {
+  const double q = z * ri;
+  return fma(fma(-q, r, z), ri, q);
+}
+
 // Back substitution R x = z, column-oriented as LAPACK's dtrsv ('U', 'N'):
 // for c = K-1 .. 0: x_c = z_c / R_cc, then z_i -= R_ic x_c for i < c.
 // Column c of R is staged through shared memory (cbuf, two 96-double
@@ -395,8 +403,11 @@ __device__ __forceinline__ void gw_solve(const double (&a)[MR], double rdiag, co
     }
     const double zct = __shfl_sync(0xffffffffu, (c >> 5) == 2 ? zt2 : ((c >> 5) ? zt1 : zt0), c & 31);
     const double zcs = __shfl_sync(0xffffffffu, (c >> 5) ? zs1 : zs0, c & 31);
-    const double vt = zct / rcc;
-    const double vs = c < s ? zcs / rcc : 0.0;
+    // x = z / R_cc: the reciprocal's Newton step and one residual correction
+    // (the division's own refinement, off the 100-cycle DDIV path)
+    double ri = __drcp_rn(rcc);
+    const double vt = gw_div(zct, rcc, ri);
+    const double vs = c < s ? gw_div(zcs, rcc, ri) : 0.0;
     if (owner < 0) {
       if (lane == 0) xpre[c] = vt;
       if (c == 0) x0s = vs;
@@ -422,6 +433,7 @@ template <int MR>
 __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs a, GwSpill sp) {
   if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
   extern __shared__ __align__(16) unsigned char smraw[];
+  hcs_smem_poison(smraw, a.smem_bytes);
   const int N = a.N, M = a.M;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const GwLayout L = gw_layout(M);
@@ -585,6 +597,7 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
         // 0..31; pre-columns (e = K - 32) to the warp's scratch P, factored in place
         const int e = K > 32 ? K - 32 : 0;
         const int e0 = K > kWarpCols ? e : 0;
+        HCS_CHECK(a.err, K >= 1 && K <= kWarpMaxK && K - e0 <= kWarpCols && (long long)e * M <= sp.pre_stride);
         for (int c = e0; c < K; ++c) {
           const double* col = a.basis_t + (size_t)gb.cols[c] * N;
           for (int i = lane; i < M; i += 32) cp_async8(orig + (c - e0) * L.ldc + i, col + gb.msk[i]);
@@ -725,6 +738,10 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
     }
     __syncwarp();
   }
+#ifdef HCS_CHECKS
+  if (a.selftest && blockIdx.x == 0 && threadIdx.x == 0) smraw[a.smem_bytes + 8] ^= 1;   // positive control
+#endif
+  hcs_smem_canary(smraw, a.smem_bytes, a.err);
 }
 
 bool gomp_warp_supported(int N, int M, int kappa) {
@@ -735,7 +752,7 @@ bool gomp_warp_supported(int N, int M, int kappa) {
 size_t gomp_warp_smem(int M, int* warps) {
   const GwLayout L = gw_layout(M);
   int w = kGwWarps;
-  while (w > 1 && L.bytes * w > 227 * 1024) --w;
+  while (w > 1 && L.bytes * w + kSmemExtra > 227 * 1024) --w;
   *warps = w;
   return L.bytes * w;
 }
@@ -743,9 +760,12 @@ size_t gomp_warp_smem(int M, int* warps) {
 template <int MR>
 static cudaError_t launch_gw_t(const GreedyArgs& args, const GwSpill& sp, int grid, int warps, size_t smem,
                                cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(gomp_warp_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(gomp_warp_kernel<MR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(smem + kSmemExtra));
   if (e != cudaSuccess) return e;
-  gomp_warp_kernel<MR><<<grid, 32 * warps, smem, stream>>>(args, sp);
+  GreedyArgs ga = args;
+  ga.smem_bytes = (unsigned)smem;
+  gomp_warp_kernel<MR><<<grid, 32 * warps, smem + kSmemExtra, stream>>>(ga, sp);
   return cudaGetLastError();
 }
 

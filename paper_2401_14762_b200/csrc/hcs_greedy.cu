@@ -134,6 +134,8 @@ template <int ALGO>
 __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a) {
   if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
   extern __shared__ __align__(16) unsigned char smraw[];
+  hcs_smem_poison(smraw, a.smem_bytes);
+  HCS_CHECK(a.err, blockIdx.x < a.slots);   // one global LS scratch slot per CTA
   const int N = a.N, M = a.M;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int kalloc = a.kalloc;
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   const double* ls_b = S;
   auto solve = [&](const uint8_t* cols, int K) {
     const bool shared_b = K <= kalloc;
+    HCS_CHECK(a.err, K >= 1 && K <= M + 1 && K <= kMaxN);
     double* B = shared_b ? S : Bglob;
     ls_shared = shared_b;
     ls_b = B;
@@ -545,6 +548,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   if (tid == 0)
     for (int k = 0; k < 15; ++k) atomicAdd(&g_phase[k], (unsigned long long)hcs_ph[k]);
 #endif
+  hcs_smem_canary(smraw, a.smem_bytes, a.err);
 }
 
 size_t greedy_smem_bytes(int M, int kalloc) { return greedy_layout(M, kalloc).bytes; }
@@ -572,9 +576,12 @@ size_t greedy_ls_doubles(int M) { return (size_t)ls_doubles(M, M) + (size_t)csne
 
 template <int ALGO>
 static cudaError_t launch_t(const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(smem + kSmemExtra));
   if (e != cudaSuccess) return e;
-  greedy_kernel<ALGO><<<grid, kGreedyThreads, smem, stream>>>(args);
+  GreedyArgs ga = args;
+  ga.smem_bytes = (unsigned)smem;
+  greedy_kernel<ALGO><<<grid, kGreedyThreads, smem + kSmemExtra, stream>>>(ga);
   return cudaGetLastError();
 }
 
@@ -587,9 +594,9 @@ cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t sme
 template <int ALGO>
 static int blocks_t(size_t smem) {
   // the dynamic shared-memory limit must be raised before the occupancy query
-  cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(greedy_kernel<ALGO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + kSmemExtra));
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<ALGO>, kGreedyThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, greedy_kernel<ALGO>, kGreedyThreads, smem + kSmemExtra);
   return nb;
 }
 

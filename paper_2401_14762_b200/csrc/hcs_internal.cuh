@@ -26,6 +26,7 @@ struct ConvexArgs {
   const long long* plist = nullptr;
   const unsigned long long* plist_n = nullptr;
   int kskip = 1;          // fista: skip the all-zero k-steps of Psi x_{k+1} (bitwise-identical)
+  unsigned smem_bytes = 0;   // dynamic shared bytes of the layout (checked builds: poison / canary)
 };
 
 struct GreedyArgs {
@@ -50,6 +51,9 @@ struct GreedyArgs {
   // the CTA kernel then works on plist[0 .. *plist_n) instead of 0 .. P-1
   const long long* plist = nullptr;
   const unsigned long long* plist_n = nullptr;
+  unsigned smem_bytes = 0;   // dynamic shared bytes of the layout (checked builds: poison / canary)
+  long long slots = 0;       // CTA scratch slots in gscratch
+  int selftest = 0;          // checked builds: 1 = deliberately overrun the shared region (positive control)
 };
 
 // spill list of the warp-per-pixel gOMP kernel
