@@ -62,6 +62,9 @@ CASES += [
     ("cfg5", "scaling", "cosamp", dict(kappa=33), 2000),
     ("cfg5", "scaling", "fista", dict(lam=100.0), 5000),
     ("cfg5", "scaling", "fista", dict(lam=0.1), 5000),
+    ("cfg5", "scaling", "admm", dict(lam=100.0, alpha=1.8), 5000),
+    ("cfg5", "scaling", "admm", dict(lam=0.1, alpha=1.8), 5000),
+    ("cfg5", "scaling", "cosamp", dict(kappa=27), 2000),
 ]
 SLOW = {("salinas", "admm", 0.1)}
 
