@@ -499,21 +499,24 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
 #pragma unroll
       for (int c = 0; c < 8; ++c) p[c] = 0.0;
       {
+        // four measured rows per step: 32 independent L2 loads in flight per
+        // lane (the same FMA order as one row at a time)
         int j = 0;
-        for (; j + 1 < M; j += 2) {
-          const double r0 = rs[j], r1 = rs[j + 1];
-          const double* row0 = a.basis + (size_t)gb.msk[j] * N + lane;
-          const double* row1 = a.basis + (size_t)gb.msk[j + 1] * N + lane;
-          double b0[8], b1[8];
+        for (; j + 3 < M; j += 4) {
+          double b[4][8], rr[4];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            b0[c] = lane + 32 * c < N ? __ldg(row0 + 32 * c) : 0.0;
-            b1[c] = lane + 32 * c < N ? __ldg(row1 + 32 * c) : 0.0;
+          for (int u = 0; u < 4; ++u) {
+            rr[u] = rs[j + u];
+            const double* row = a.basis + (size_t)gb.msk[j + u] * N + lane;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) b[u][c] = lane + 32 * c < N ? __ldg(row + 32 * c) : 0.0;
           }
 #pragma unroll
-          for (int c = 0; c < 8; ++c) p[c] = fma(b1[c], r1, fma(b0[c], r0, p[c]));
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) p[c] = fma(b[u][c], rr[u], p[c]);
         }
-        if (j < M) {
+        for (; j < M; ++j) {
           const double r0 = rs[j];
           const double* row0 = a.basis + (size_t)gb.msk[j] * N + lane;
 #pragma unroll

@@ -369,11 +369,13 @@ def test_admm_zero_shrinkage_pass_matches_oracle(lam):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["fista", "admm"])
 @pytest.mark.parametrize("lam", [0.1, 0.01, 100.0])
-def test_fista_kstep_skip_bitwise(monkeypatch, lam):
-    """FISTA's second GEMM (Psi x_{k+1}) skips the k-steps whose four
-    coefficient rows are zero in every slot: the skipped products are exact
-    zeros, so results are bit-for-bit those of the dense GEMM."""
+def test_fista_kstep_skip_bitwise(monkeypatch, algo, lam):
+    """The sparse GEMMs (FISTA's Psi x_{k+1}, ADMM's Psi z) skip the DMMAs
+    whose 4 x 8 block of input (four coefficient rows of an 8-slot column
+    block) is zero: the skipped products are exact zeros, so results are
+    bit-for-bit those of the dense GEMM."""
     import torch
     from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
     c = synth.generate(6, 50, 224, seed=44)
@@ -383,8 +385,8 @@ def test_fista_kstep_skip_bitwise(monkeypatch, lam):
     outs = []
     for flag in ("0", "1"):
         monkeypatch.setenv("HCS_CONVEX_KSKIP", flag)
-        b = solve_batch("fista", *args)
+        b = solve_batch(algo, *args)
         torch.cuda.synchronize()
-        outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.final_delta, b.converged)])
+        outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.final_delta, b.converged, b.admm_gap)])
     for u, v in zip(*outs):
-        assert np.array_equal(u, v)
+        assert np.array_equal(u, v, equal_nan=True)

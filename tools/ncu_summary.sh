@@ -9,10 +9,11 @@ import csv, sys
 rows = list(csv.reader(sys.stdin))
 hdr, units, vals = rows[0], rows[1], rows[2:]
 want = ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active", "sm__inst_executed_pipe_fp64",
-        "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak", "gpu__time_duration.sum", "sm__pipe_tensor")
+        "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak", "gpu__time_duration.sum")
+sub = ("pipe_tensor_cycles_active", "subpipe_dmma", "lts__t_sectors.sum", "lts__throughput")
 for v in vals:
     for i, h in enumerate(hdr):
-        if any(h.startswith(w) for w in want):
+        if any(h.startswith(w) for w in want) or any(w in h for w in sub):
             print(h, units[i], v[i])
 '
 echo "--- top source lines (warp stall samples)"
