@@ -45,11 +45,6 @@ bool greedy(int algo) { return algo == HCS_GOMP || algo == HCS_BIHT || algo == H
 constexpr size_t kGreedySmemCap = 200 * 1024;
 constexpr int kMaxGreedyPerSm = 8;
 
-// ADMM: the slot engine's signal-domain dual W, 16 doubles per thread, for the
-// largest grid (one 512-thread or two 256-thread CTAs per SM)
-constexpr int kWscrPerThread = 16;
-inline size_t admm_wscr_bytes(int sms) { return align256(sizeof(double) * kWscrPerThread * 512 * (size_t)sms); }
-
 // Greedy workspace (ABI 1.1): [header 256 B: queue counter, error flag,
 // spill count, spill-queue counter][transposed basis N x N doubles][spill
 // list P x int64][per-CTA LS scratch, greedy_ls_doubles(M) doubles per CTA]
@@ -92,7 +87,6 @@ size_t hcs_workspace_bytes(int algo, int64_t P, int32_t N, int32_t M) {
     b += align256(sizeof(double) * (size_t)Np);            // u0
     if (algo == HCS_FISTA && P > 0) b += align256(sizeof(double) * (size_t)P);   // Lipschitz constants
     if (algo == HCS_ADMM && P > 0) b += align256(sizeof(long long) * (size_t)P);  // uncertified-pixel list
-    if (algo == HCS_ADMM) b += admm_wscr_bytes(num_sms());                        // dual W scratch
   } else if (greedy(algo)) {
     b = greedy_ws(P, N, M, 0).scratch;
     // per-CTA global scratch for systems beyond the shared-memory region
@@ -186,21 +180,10 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
       if (e != cudaSuccess) return cuda_fail(e, "admm_zero_kernel");
       args.plist = plist;
       args.plist_n = plist_n;
-      // the W scratch follows the pixel list; its size bounds the grid below
-      args.wscr = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(plist) +
-                                            align256(sizeof(long long) * (size_t)P));
     }
     // persistent: one CTA (32 slots) or two CTAs (16 slots each) per SM
     const long long tiles = (P + slots - 1) / slots;
-    long long ctas = (long long)sms * hcs::convex_ctas_per_sm(calgo, Np, M, slots);
-    if (algo == HCS_ADMM) {   // never more threads than the W scratch holds (sized on the workspace's device)
-      const size_t used = reinterpret_cast<unsigned char*>(args.wscr) - ws;
-      const long long threads = workspace_bytes > used ? (long long)((workspace_bytes - used) /
-                                                                     (sizeof(double) * kWscrPerThread)) : 0;
-      const long long per_cta = slots == 32 ? 512 : 256;
-      if (ctas > threads / per_cta) ctas = threads / per_cta;
-      if (ctas < 1) return fail(HCS_EINVAL, "workspace too small");
-    }
+    const long long ctas = (long long)sms * hcs::convex_ctas_per_sm(calgo, Np, M, slots);
     const int grid = (int)(tiles < ctas ? tiles : ctas);
     e = hcs::launch_convex(calgo, args, slots, grid, stream);
     if (e != cudaSuccess) return cuda_fail(e, "convex_kernel");

@@ -37,12 +37,6 @@ enum { kEmpty = 0, kActive = 1 };
 __device__ unsigned long long g_phase_cx[16];
 #endif
 
-// the per-block masked GEMM when it skips at least an eighth of the dense DMMAs
-__device__ __forceinline__ bool gemm_sparse_pays(const unsigned long long* km, int KS) {
-  const int act = __popcll(km[0]) + __popcll(km[1]) + __popcll(km[2]) + __popcll(km[3]);
-  return 8 * act <= 7 * 4 * KS;
-}
-
 template <int SL>
 struct SlotState {
   long long pid[SL];
@@ -52,15 +46,11 @@ struct SlotState {
   double slip[SL];        // its Lipschitz constant (fista)
   double t[SL], tn[SL], betan[SL];
   double inv_l[SL], thr[SL];
-  int status[SL], iter[SL], flag[SL], rfail[SL], retired[SL], moff[SL], need_pf[SL], wfresh[SL];
+  int status[SL], iter[SL], flag[SL], rfail[SL], retired[SL], moff[SL], need_pf[SL];
   int nact[2];
   int exhausted;
   long long np;           // pixels in the queue (P, or *plist_n)
-  // k-steps (4 rows) of the sparse GEMM input with a nonzero in some slot of
-  // each 8-slot column block, by tick parity: fista x_{k+1} (set by epilogue
-  // 1, read by GEMM 2 of the same tick), admm z (set by epilogue 2, read by
-  // GEMM 1 of the next tick)
-  unsigned long long kmask[2][4];
+  unsigned long long kmask;   // fista: k-steps of x_{k+1} with a nonzero in some slot
 };
 
 // Slot-column layout of the GEMM input buffers: 32 slots (one CTA per SM) or 16
@@ -127,7 +117,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
   uint8_t* ps = pos + s * kMaxN;
   for (int n = lane; n < Np; n += 32) {
     bufA[slot_idx<SL>(n, s)] = 0.0;
-    bufB[slot_idx<SL>(n, s)] = 0.0;   // fista z_0 = 0; admm X_0 = Psi x_0 = 0 (W recursion)
+    if (ALGO == kFista) bufB[slot_idx<SL>(n, s)] = 0.0;   // z_0 = 0
   }
   for (;;) {
     cp_async_wait_all();
@@ -197,7 +187,6 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
       ss.pid[s] = pid;
       ss.start[s] = t0;
       ss.status[s] = kActive;
-      ss.wfresh[s] = 1;   // admm: the slot's dual W starts at 0 (no read of the stale scratch)
       ss.iter[s] = 0;
       ss.t[s] = 1.0;
       if (ALGO == kFista) {
@@ -279,7 +268,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // SL * 256: row -> measurement index
   uint8_t* sm = pos + SL * kMaxN;                       // SL * stage_mask_bytes(M) staged mask rows
   const int cred = (SL == 32) ? col_of_reduced(lane) : col_of_reduced4(lane);
-  const bool use_kskip = (SL == 32) && a.kskip;
+  const bool use_kskip = (SL == 32) && ALGO == kFista && a.kskip;
 
   double p0[MAXRB][CB][2], p1[MAXRB][CB][2];
 #pragma unroll
@@ -293,7 +282,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     ss.retired[threadIdx.x] = 0;
     ss.need_pf[threadIdx.x] = 0;
   }
-  if (threadIdx.x < 8) ss.kmask[threadIdx.x >> 2][threadIdx.x & 3] = 0ull;
   if (threadIdx.x == 0) {
     ss.exhausted = 0;
     ss.nact[0] = ss.nact[1] = 0;
@@ -344,7 +332,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       if (hl == 0 && valid) {
         ss.retired[s] = 0;
-        ss.wfresh[s] = 0;
         if (was_active) {
           if (ALGO == kFista) ss.t[s] = ss.tn[s];
           finish_iteration<SL>(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
@@ -377,10 +364,10 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       __syncwarp();
     }
-    if (threadIdx.x == 0) ss.nact[par ^ 1] = 0;
-    // masks filled this tick: fista's (epilogue 1 -> GEMM 2) at par, admm's
-    // (epilogue 2 -> next tick's GEMM 1) at par ^ 1
-    if (threadIdx.x < 4) ss.kmask[ALGO == kFista ? par : par ^ 1][threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) {
+      ss.nact[par ^ 1] = 0;
+      ss.kmask = 0ull;
+    }
     __syncthreads();
     CMARK(0);
     for (int s = w; s < SL; s += W)
@@ -413,18 +400,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     CMARK(1);
 
     double part[NV];
-    unsigned long long kbits[CB];      // k-steps of this thread's nonzero sparse-input entries, per column block
-#pragma unroll
-    for (int cb = 0; cb < CB; ++cb) kbits[cb] = 0ull;
-    // OR of kbits over the warp into the CTA-wide per-block masks
-    auto publish = [&](unsigned long long* km) {
-#pragma unroll
-      for (int cb = 0; cb < CB; ++cb) {
-        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits[cb]);
-        const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits[cb] >> 32));
-        if (lane == 0 && (lo | hi)) atomicOr(&km[cb], ((unsigned long long)hi << 32) | lo);
-      }
-    };
+    unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
     if (ALGO == kFista) {
       // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
       gemm(a.fragT, bufA);
@@ -448,19 +424,23 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             p0[rb][cb][i] = xn;
             bad |= !isfinite(xn);
             bufA[zi] = xn;
-            if (xn != 0.0) kbits[cb] |= 1ull << ((row0 + 8 * rb) >> 2);
+            if (xn != 0.0) kbits |= 1ull << ((row0 + 8 * rb) >> 2);
           }
           if (bad) ss.flag[s] = 1;
         }
-      if (use_kskip) publish(ss.kmask[par]);
+      if (use_kskip) {
+        const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits);
+        const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits >> 32));
+        if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask, ((unsigned long long)hi << 32) | lo);
+      }
       preload(mat2);   // next GEMM's first k-steps (the dense path's)
       __syncthreads();
       CMARK(3);
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
-      // only the DMMAs whose 4 x 8 block of x_{k+1} has a nonzero (the masked
-      // loop when it saves at least an eighth of the dense DMMAs)
-      if (use_kskip && gemm_sparse_pays(ss.kmask[par], KS)) {
-        if constexpr (SL == 32) tile_gemm_cbmask(nrb, a.fragS, rb0, bufA, KS, ss.kmask[par], acc);
+      // the masked loop only when at most half the k-steps are active (it
+      // prefetches 2 steps ahead instead of 4: slower on a dense mask)
+      if (use_kskip && 2 * __popcll(ss.kmask) <= KS) {
+        if constexpr (SL == 32) tile_gemm_masked(nrb, a.fragS, rb0, bufA, KS, ss.kmask, acc);
       } else {
         gemm(a.fragS, bufA);
       }
@@ -497,16 +477,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       __syncthreads();
       CMARK(5);
     } else {
-      // ---- GEMM 1: Z = Psi z (z sparse: soft-thresholded); epilogue: the
-      //      signal-domain dual W = Psi w = W_prev + X - Z (W in p0, X = Psi x
-      //      of the last pass in bufB), v = Psi (z - w) = Z - W,
-      //      u' = (yhat + alpha v) / (d + alpha), residual y - A x = y - u'[mask]
-      //      of this iteration's x ----------------------------------------------
-      if (use_kskip && gemm_sparse_pays(ss.kmask[par], KS)) {
-        if constexpr (SL == 32) tile_gemm_cbmask(nrb, a.fragS, rb0, bufA, KS, ss.kmask[par], acc);
-      } else {
-        gemm(a.fragS, bufA);
-      }
+      // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
+      //      residual y - A x = y - u'[mask] of this iteration's x ----------
+      gemm(a.fragS, bufA);
       CMARK(2);
       const double alpha = a.prm.alpha;
       // 1 / (d + alpha) for d = 0, 1 (Psi orthonormal: the factor's eigenvalues)
@@ -524,16 +497,8 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             const int pj = pos[s * kMaxN + n];
             const bool in_mask = pj != 0xFF;
             const double yh = in_mask ? ys[s * M + pj] : 0.0;
-            const int bi = slot_idx<SL>(n, s);
-            const double Z = acc[rb][cb][i];
-            // W lives in a per-thread L2-resident scratch (coalesced per warp):
-            // registers would spill at 512 threads x 128
-            double* wp = a.wscr + ((size_t)blockIdx.x * (MAXRB * CB * 2) + (rb * CB + cb) * 2 + i) * blockDim.x +
-                         threadIdx.x;
-            const double W = (ss.wfresh[s] ? 0.0 : *wp + bufB[bi]) - Z;   // W_k = W_{k-1} + X_k - Z_k
-            *wp = W;
-            const double up = (yh + alpha * (Z - W)) * (in_mask ? inv1 : inv0);
-            bufB[bi] = up;
+            const double up = (yh + alpha * acc[rb][cb][i]) * (in_mask ? inv1 : inv0);
+            bufB[slot_idx<SL>(n, s)] = up;
             if (in_mask) {
               const double rn = yh - up;
               const double d = rn - r[s * M + pj];
@@ -571,8 +536,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             // it needs no registers between passes
             if (act && n < N) xo[n] = zn;
             p1[rb][cb][i] = wn;
-            bufA[slot_idx<SL>(n, s)] = zn;                                // next GEMM 1 input (sparse)
-            if (zn != 0.0) kbits[cb] |= 1ull << (n >> 2);
+            bufA[slot_idx<SL>(n, s)] = zn - wn;                           // next GEMM 1 input
             const double dg = x - zn;
             g2 += dg * dg;
             bad |= !isfinite(zn);
@@ -581,7 +545,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
           if (bad) ss.flag[s] = 1;
         }
       partG[w * SL + cred] = reduce(part);
-      if (use_kskip) publish(ss.kmask[par ^ 1]);
       preload(mat1);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(5);

@@ -268,84 +268,6 @@ __device__ __forceinline__ void tile_gemm_masked(int nrb, const double* frag, in
   else tile_gemm_masked<1>(frag, rb0, In, KS, kmask, acc);
 }
 
-// acc = Mat(row blocks rb0 ..) * In with a k-step mask PER 8-COLUMN BLOCK:
-// bit ks of km[cb] set iff rows 4 ks .. 4 ks + 3 of In are nonzero in some of
-// the block's 8 columns.  DMMAs whose B fragment is all zero are skipped
-// (bitwise the dense result: a * 0 = +-0 leaves every partial sum unchanged,
-// and each accumulator still adds its k-steps in ascending order); A
-// fragments are loaded only for the k-steps some block needs, three active
-// k-steps ahead.  The slot engine's sparse inputs (FISTA's x_{k+1}, ADMM's z)
-// are soft-thresholded, and per 8-pixel block the union of their supports is
-// far smaller than per 32 (young pixels' dense iterates spoil one block, not
-// all four): 40% (FISTA) and 58% (ADMM) of the dense DMMAs on the scaling
-// cube's tile (tools/sparsity_study.py).
-template <int NRB>
-__device__ __forceinline__ void tile_gemm_cbmask(const double* __restrict__ frag, int rb0, const double* In, int KS,
-                                                 const unsigned long long* km, double (&acc)[2][4][2]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int rb = 0; rb < NRB; ++rb)
-#pragma unroll
-    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
-  const unsigned long long m0 = km[0], m1 = km[1], m2 = km[2], m3 = km[3];
-  unsigned long long m = m0 | m1 | m2 | m3;
-  auto next = [&](unsigned long long& mm) -> int {
-    if (!mm) return -1;
-    const int ks = __ffsll((long long)mm) - 1;
-    mm &= mm - 1;
-    return ks;
-  };
-  auto load = [&](int ks) -> double2 {
-    double2 v = make_double2(0.0, 0.0);
-    if (ks < 0) return v;
-    if (NRB == 2) {
-      v = __ldg(reinterpret_cast<const double2*>(frag + (size_t)rb0 * KS * 32) + lane + ks * 32);
-    } else {
-      v.x = __ldg(frag + (size_t)rb0 * KS * 32 + lane + ks * 32);
-    }
-    return v;
-  };
-  int k0 = next(m), k1 = next(m), k2 = next(m);
-  double2 a0 = load(k0), a1 = load(k1), a2 = load(k2);
-  while (k0 >= 0) {
-    const int k3 = next(m);
-    const double2 a3 = load(k3);
-    const double* b = In + (k0 << 7) + lane;
-    const unsigned long long bit = 1ull << k0;
-    if (m0 & bit) {
-      const double b0 = b[0];
-      dmma(acc[0][0], a0.x, b0);
-      if (NRB == 2) dmma(acc[1][0], a0.y, b0);
-    }
-    if (m1 & bit) {
-      const double b1 = b[32];
-      dmma(acc[0][1], a0.x, b1);
-      if (NRB == 2) dmma(acc[1][1], a0.y, b1);
-    }
-    if (m2 & bit) {
-      const double b2 = b[64];
-      dmma(acc[0][2], a0.x, b2);
-      if (NRB == 2) dmma(acc[1][2], a0.y, b2);
-    }
-    if (m3 & bit) {
-      const double b3 = b[96];
-      dmma(acc[0][3], a0.x, b3);
-      if (NRB == 2) dmma(acc[1][3], a0.y, b3);
-    }
-    k0 = k1;
-    a0 = a1;
-    k1 = k2;
-    a1 = a2;
-    k2 = k3;
-    a2 = a3;
-  }
-}
-__device__ __forceinline__ void tile_gemm_cbmask(int nrb, const double* frag, int rb0, const double* In, int KS,
-                                                 const unsigned long long* km, double (&acc)[2][4][2]) {
-  if (nrb == 2) tile_gemm_cbmask<2>(frag, rb0, In, KS, km, acc);
-  else tile_gemm_cbmask<1>(frag, rb0, In, KS, km, acc);
-}
-
 // ---------------------------------------------------------------------------
 // Half-width engine (two CTAs per SM, 16 slots, 8 warps): the same GEMM with
 // CB = 2 column blocks and up to 4 row blocks per warp, so that the two CTAs

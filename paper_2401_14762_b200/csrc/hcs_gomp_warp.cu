@@ -748,8 +748,10 @@ __global__ void __launch_bounds__(32 * kGwWarps, 1) gomp_warp_kernel(GreedyArgs 
 }
 
 bool gomp_warp_supported(int N, int M, int kappa) {
-  // pre-column scratch: up to 32 columns of M rows per warp in a CTA scratch slot
-  return M >= 1 && M <= 96 && kappa <= kWarpCols && N <= kMaxN && 64 * (size_t)M <= greedy_ls_doubles(M);
+  // pre-column scratch: the columns beyond the 32 lanes (K <= M, so at most
+  // M - 32 of them) of M rows each per warp, in a CTA scratch slot
+  const size_t pre = M > 32 ? (size_t)(M - 32) : 0;
+  return M >= 1 && M <= 96 && kappa <= kWarpCols && N <= kMaxN && pre * (size_t)M <= greedy_ls_doubles(M);
 }
 
 size_t gomp_warp_smem(int M, int* warps) {

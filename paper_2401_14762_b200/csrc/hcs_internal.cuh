@@ -25,8 +25,7 @@ struct ConvexArgs {
   // certify): the engine works on plist[0 .. *plist_n) instead of 0 .. P-1
   const long long* plist = nullptr;
   const unsigned long long* plist_n = nullptr;
-  int kskip = 1;          // skip the DMMAs of all-zero 4 x 8 blocks of the sparse GEMM input (bitwise)
-  double* wscr = nullptr;   // admm: per-thread scratch of the signal-domain dual W (16 doubles per thread)
+  int kskip = 1;          // fista: skip the all-zero k-steps of Psi x_{k+1} (bitwise-identical)
   unsigned smem_bytes = 0;   // dynamic shared bytes of the layout (checked builds: poison / canary)
 };
 

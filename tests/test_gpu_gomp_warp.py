@@ -84,7 +84,7 @@ def test_rank_deficient_refits_take_the_minimum_norm_path():
 
 
 def test_flags_budget_and_cap():
-    basis, y, masks = _cube(224, 90, 64, seed=5)
+    basis, y, masks = _cube(224, 90, 60, seed=5)
     y = y.copy()
     y[3] = 0.0                  # y = 0 shortcut: converged, 0 iterations
     dev = torch.device("cuda")
@@ -93,13 +93,13 @@ def test_flags_budget_and_cap():
                     torch.as_tensor(basis, device=dev), cfg)
     it = b.iterations.cpu().numpy()
     assert it[3] == 0 and bool(b.converged[3].item())
-    assert np.all(np.delete(it, 3) == 1) and not b.converged.cpu().numpy()[np.arange(64) != 3].any()
+    assert np.all(np.delete(it, 3) == 1) and not b.converged.cpu().numpy()[np.arange(60) != 3].any()
     # an expired budget: every pixel stops before its first pass (timeout, not converged)
     cfg = SolverConfig(kappa=27, atoms_per_iter=5, time_limit=1e-9, max_iter=100)
     b = solve_batch("gomp", torch.as_tensor(y, device=dev), torch.as_tensor(masks, device=dev),
                     torch.as_tensor(basis, device=dev), cfg)
     it = b.iterations.cpu().numpy()
-    assert np.all(np.delete(it, 3) == 0) and not b.converged.cpu().numpy()[np.arange(64) != 3].any()
+    assert np.all(np.delete(it, 3) == 0) and not b.converged.cpu().numpy()[np.arange(60) != 3].any()
     # non-finite measurements: ValueError, as scipy's finiteness check in the reference
     y[7, 2] = np.nan
     with pytest.raises(ValueError):
