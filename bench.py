@@ -242,7 +242,7 @@ def _ncu_traffic(convex, algo, lab, pixels, n):
     committed ncu --set full capture of that launch (profiles/), when it
     covers this kernel, configuration and cube size; else None."""
     try:
-        rec = json.loads((ROOT / "profiles" / "ncu_traffic_r01.json").read_text())["kernels"]
+        rec = json.loads((ROOT / "profiles" / "ncu_traffic_r02.json").read_text())["kernels"]
     except (OSError, ValueError, KeyError):
         return None
     key = (("convex_kernel<%s>" if convex else "greedy_kernel<%s>") % algo) + "|" + lab
