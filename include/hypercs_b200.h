@@ -115,7 +115,11 @@ const char* hcs_last_error(void);
 /* Device workspace hcs_recover needs for (algo, P, N, M), sized for the
  * device current at this call.  Layout (ABI 1.1; opaque to callers): a 256 B
  * header (work-queue counters, the error word hcs_recover_status reads, the
- * spill count of the warp-per-pixel gOMP kernel); FISTA / ADMM: the basis in
+ * spill count of the warp-per-pixel gOMP kernel, and for the greedy solvers a
+ * word that is 0 iff the basis was recognised on the device as the
+ * orthonormal DCT-II, which lets BIHT / CoSaMP form their least-squares Gram
+ * matrices in closed form; any other orthonormal basis takes the general
+ * path); FISTA / ADMM: the basis in
  * DMMA fragment order (twice), a start vector, per-pixel Lipschitz constants
  * or the ADMM pixel list; gOMP / BIHT / CoSaMP: the transposed basis, a
  * P-entry spill list and per-CTA least-squares scratch (hcs_recover never

@@ -190,7 +190,7 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
     return HCS_OK;
   }
   const int kalloc = hcs::greedy_kalloc_host(algo, M, prm->kappa, kGreedySmemCap);
-  const size_t smem = hcs::greedy_smem_bytes(M, kalloc);
+  const size_t smem = hcs::greedy_smem_bytes(algo, M, kalloc);
   int per_sm = hcs::greedy_blocks_per_sm(algo, M, smem);
   if (const char* ov = getenv("HCS_GREEDY_PER_SM")) {   // diagnostics override
     const int v = atoi(ov);
@@ -206,10 +206,15 @@ int hcs_recover(int algo, int64_t P, int32_t N, int32_t M, const double* basis, 
   double* basis_t = reinterpret_cast<double*>(ws + gw.basis_t);
   long long* spill_list = reinterpret_cast<long long*>(ws + gw.spill);
   double* gscratch = reinterpret_cast<double*>(ws + gw.scratch);
-  e = hcs::launch_transpose_basis(basis, N, basis_t, stream);
+  int* notdct = reinterpret_cast<int*>(ws + 32);   // header word: 0 = DCT-II basis (closed-form CSNE Gram)
+  e = hcs::launch_transpose_basis(basis, N, basis_t, notdct, stream);
   if (e != cudaSuccess) return cuda_fail(e, "transpose_basis_kernel");
   hcs::GreedyArgs args{(long long)P, N, M, kalloc, basis, y, mask, x_out, st, pr, counter, err, gscratch, basis_t};
   args.slots = gw.slots;
+  args.notdct = notdct;
+  if (const char* ov = getenv("HCS_DCT_GRAM")) {   // A/B experiments: 0 = always the DMMA Gram
+    if (atoi(ov) == 0) args.notdct = nullptr;
+  }
 #ifdef HCS_CHECKS
   if (const char* ov = getenv("HCS_CHECK_SELFTEST")) args.selftest = atoi(ov);
 #endif

@@ -166,27 +166,36 @@ __device__ __forceinline__ void gw_copy_chunk(const double (&a)[MR], double2* v2
   }
 }
 
-// d = sum_{rows >= 4 (j / 4)} v_i a_i  (v is zero on the rows below j)
+// d = sum_i v_i a_i and a_i -= f v_i over the rows >= 16 (j / 16): v is zero
+// on every row below j (gw_qr keeps the finished rows of vb cleared), so the
+// extra terms add exact zeros and leave the finished rows of a (R) unchanged,
+// bit for bit what a loop from row j would give.  Entering the row loop at a
+// 4-row chunk made every chunk its own basic block with the latency of its
+// two shared loads exposed (45% of the kernel's stall samples,
+// ncu_gomp_warp27_r02_v16); 16-row groups issue eight loads ahead of their
+// FMAs (all rows straight-line spills: the column fills the register file).
+#define GW_GROUPS(X) X(0) X(1) X(2) X(3) X(4) X(5)
 template <int MR>
 __device__ __forceinline__ double gw_dot(const double (&a)[MR], const double* vb, int j) {
   double d[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const double2* v2 = reinterpret_cast<const double2*>(vb);
-  switch (j >> 2) {
-#define GW_DOT_CASE(k) case k: gw_dot_chunk<MR, k>(a, v2, d);
-    GW_CASES(GW_DOT_CASE)
+  switch (j >> 4) {
+#define GW_DOT_CASE(g) case g: gw_dot_chunk<MR, 4 * g>(a, v2, d); gw_dot_chunk<MR, 4 * g + 1>(a, v2, d); \
+                               gw_dot_chunk<MR, 4 * g + 2>(a, v2, d); gw_dot_chunk<MR, 4 * g + 3>(a, v2, d);
+    GW_GROUPS(GW_DOT_CASE)
 #undef GW_DOT_CASE
     default: break;
   }
   return ((d[0] + d[4]) + (d[1] + d[5])) + ((d[2] + d[6]) + (d[3] + d[7]));
 }
 
-// a_i -= f v_i on the rows >= 4 (j / 4)
 template <int MR>
 __device__ __forceinline__ void gw_update(double (&a)[MR], const double* vb, int j, double f) {
   const double2* v2 = reinterpret_cast<const double2*>(vb);
-  switch (j >> 2) {
-#define GW_UPD_CASE(k) case k: gw_upd_chunk<MR, k>(a, v2, f);
-    GW_CASES(GW_UPD_CASE)
+  switch (j >> 4) {
+#define GW_UPD_CASE(g) case g: gw_upd_chunk<MR, 4 * g>(a, v2, f); gw_upd_chunk<MR, 4 * g + 1>(a, v2, f); \
+                               gw_upd_chunk<MR, 4 * g + 2>(a, v2, f); gw_upd_chunk<MR, 4 * g + 3>(a, v2, f);
+    GW_GROUPS(GW_UPD_CASE)
 #undef GW_UPD_CASE
     default: break;
   }
@@ -295,7 +304,7 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
     if (xn2 != 0.0) {
       beta = -copysign(sqrt(fma(al, al, xn2)), al);
       amb = al - beta;
-      g = 1.0 / (beta * (beta - al));
+      g = __drcp_rn(beta * (beta - al));   // correctly rounded, as 1.0 / x, off the DDIV path
     }
     if (owner < 0) {
       if (lane == (j & 31)) P[j * M + j] = beta;   // R_jj of the pre-column
@@ -311,8 +320,13 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
       }
       if (lane == 0) vb[j] = amb;
     } else {
-      const int j0 = j & ~3;   // v: rows j0 .. j-1 of the first chunk read -> 0, row j -> alpha - beta
+      // v: row j -> alpha - beta; rows j0 .. j-1 of its chunk (just copied: R
+      // entries of the owner) and the previous chunk (the last reflectors'
+      // v, complete once j enters a new chunk) -> 0, so that vb is zero on
+      // every row below j for the straight-line dot / update
+      const int j0 = j & ~3;
       if (lane <= j - j0) vb[j0 + lane] = (j0 + lane == j) ? amb : 0.0;
+      if (j0 == j && j >= 4 && lane >= 28) vb[j - 32 + lane] = 0.0;   // rows j-4 .. j-1
     }
     __syncwarp();
     double py = 0.0;

@@ -50,6 +50,9 @@ struct GreedyShared {
   int brk;
   int flag;
   int ctr;   // must follow flag: ls_csne's Gram tile counter (flag[1])
+  // CoSaMP: argument blocks of ls_csne in shared memory (hcs_greedy.cu: solve)
+  CsneScratch cs;
+  DctGram dg;
 };
 
 // Shared-memory layout (doubles unless noted), identical on host and device.
@@ -58,7 +61,7 @@ struct GreedyShared {
 // scratch.
 struct GreedyLayout {
   int Mp, bmax, gmax;        // padded rows; doubles for B and for the Gram tiles
-  int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring, dinv, cv;   // double offsets
+  int vec, x, ys, r, yv, sv, vn1, vn2, zt, keys, ring, dinv, cv, F, q;   // double offsets
   int ints;                  // pivoted-fallback perm (ints) offset, in doubles
   int lists;                 // uint8 support lists + mask bytes offset, in doubles
   size_t bytes;
@@ -70,6 +73,11 @@ __host__ __device__ inline int ls_doubles(int M, int K) {
   const int piv = M * ((K + 1) | 1);
   const int blk = csne_ld(M) * csne_cols(K);
   return piv > blk ? piv : blk;
+}
+
+// per-CTA global scratch: the widest system's columns and Gram tiles, F and A^T y
+__host__ __device__ inline int cta_scratch_doubles(int M) {
+  return ls_doubles(M, M) + csne_gram_doubles(M) + 2 * kMaxN;
 }
 
 __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
@@ -95,6 +103,12 @@ __host__ __device__ inline GreedyLayout greedy_layout(int M, int kalloc) {
   L.dinv = o; o += M + 9;
   L.cv = o; o += M + 9;
   L.ring = o; o += M;           // residual snapshot for exact cycle confirmation
+  // the closed-form Gram's generator F(d) and A^T y (hcs_ls_csne.cuh: DctGram)
+  // are kept in the CTA's global scratch and staged over vec / x, which are
+  // dead while a least-squares system is being solved: 4 KB more shared
+  // memory per CTA cost CoSaMP 5% through the smaller L1
+  L.F = L.vec;
+  L.q = L.x;
   L.ints = perm;
   // lists (2 x 256 uint8), msk (M bytes), then GreedyShared
   L.lists = o;
@@ -141,8 +155,9 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   const int kalloc = a.kalloc;
   const GreedyLayout L = greedy_layout(M, kalloc);
   double* S = reinterpret_cast<double*>(smraw);
-  double* Bglob = a.gscratch + (size_t)blockIdx.x * (ls_doubles(M, M) + csne_gram_doubles(M));
+  double* Bglob = a.gscratch + (size_t)blockIdx.x * cta_scratch_doubles(M);
   double* Gglob = Bglob + ls_doubles(M, M);
+  double* Fq = Gglob + csne_gram_doubles(M);   // 2 kMaxN: the pixel's F and A^T y between solves
   double* vec = S + L.vec;      // N: p / u / x_full
   double* x = S + L.x;          // N: current iterate
   double* ys = S + L.ys;        // M
@@ -177,8 +192,49 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   // there instead of re-gathering dictionary rows from L2
   bool ls_ok = false, ls_shared = true;
   const double* ls_b = S;
+  // DCT-II basis (verified by transpose_basis_kernel): closed-form Gram entries
+  const bool use_dct = ALGO == kCosamp && a.ls_mode == 0 && a.notdct != nullptr && *(volatile const int*)a.notdct == 0;
+  const double s0n = sqrt(1.0 / (double)N), s1n = sqrt(2.0 / (double)N);
+  bool f_ready = false;   // this pixel's F and y^T y are computed (at its first wide system)
+  double yty = 0.0;
   auto solve = [&](const uint8_t* cols, int K) {
     const bool shared_b = K <= kalloc;
+    // wide systems (columns in the L2 scratch) of a DCT-II basis: closed-form Gram
+    const bool dct_far = use_dct && !shared_b;
+    if (dct_far && !f_ready) {
+      // F(d) = sum_j cos(theta_{mask_j} d) = (A^T 1)[d] / s_d: the column sums of
+      // the measured rows, accumulated like the correlation; once per pixel
+      double* part = S;          // the LS region is free until the gather
+      double acc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+#pragma unroll 4
+      for (int j = warp; j < M; j += 4) {
+        const double* row = a.basis + (size_t)msk[j] * N + lane;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (lane + 32 * c < N) acc[c] += __ldg(row + 32 * c);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (lane + 32 * c < N) part[warp * kMaxN + lane + 32 * c] = acc[c];
+      double py = 0.0;
+      for (int j = tid; j < M; j += nt) py += ys[j] * ys[j];
+      __syncthreads();
+      for (int n = tid; n < N; n += nt) {
+        const double u = (part[n] + part[kMaxN + n]) + (part[2 * kMaxN + n] + part[3 * kMaxN + n]);
+        Fq[n] = u / (n ? s1n : s0n);
+      }
+      yty = cta_sum(py, g.red);
+      f_ready = true;
+      __syncthreads();
+    }
+    if (dct_far) {   // stage F and A^T y over vec / x (dead until the new iterate is built)
+      for (int n = tid; n < N; n += nt) {
+        S[L.F + n] = Fq[n];
+        S[L.q + n] = Fq[kMaxN + n];
+      }
+    }
     HCS_CHECK(a.err, K >= 1 && K <= M + 1 && K <= kMaxN);
     double* B = shared_b ? S : Bglob;
     ls_shared = shared_b;
@@ -236,13 +292,27 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         }
       }
     }
-    __syncthreads();
-    GMARK(3);
     // Gram tiles in shared memory whenever they fit the whole LS region (B then
     // lives in the global scratch), else in the global scratch too
     double* G = shared_b ? S + L.bmax : (csne_gram_doubles(K) <= L.bmax + L.gmax ? S : Gglob);
-    const CsneScratch cs{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
-    if (ls_csne(B, ldb, M, K, sv, cs, php)) {
+    bool solved;
+    if constexpr (ALGO == kCosamp) {
+      // argument blocks in shared memory: as locals they live on the stack, and
+      // with four 48 KB CTAs per SM the L1 left over does not hold the stacks
+      if (tid == 0) {
+        g.cs = CsneScratch{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
+        g.dg = DctGram{S + L.F, S + L.q, cols, N, s0n, s1n, yty};
+      }
+      __syncthreads();
+      GMARK(3);
+      solved = ls_csne<true>(B, ldb, M, K, sv, g.cs, php, dct_far ? &g.dg : nullptr);
+    } else {
+      __syncthreads();
+      GMARK(3);
+      const CsneScratch cs{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
+      solved = ls_csne<false>(B, ldb, M, K, sv, cs, php);
+    }
+    if (solved) {
       ls_ok = true;
       return;
     }
@@ -296,6 +366,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
       __syncthreads();
       continue;
     }
+    f_ready = false;
     const long long t0 = g.start;
     double delta = 1.0;
     int iters = 0, ncall = 0, ksupp = 0;
@@ -338,6 +409,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
         __syncthreads();
         for (int n = tid; n < N; n += nt) {
           double p = (part[n] + part[kMaxN + n]) + (part[2 * kMaxN + n] + part[3 * kMaxN + n]);
+          if (ALGO == kCosamp && iters == 0 && use_dct) Fq[kMaxN + n] = p;   // r = y on the first pass: A^T y (DctGram's y row)
           if (ALGO == kBiht) p = __dadd_rn(x[n], __dmul_rn(a.prm.mu, p));   // solvers.py:318
           vec[n] = p;
         }
@@ -551,7 +623,7 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
   hcs_smem_canary(smraw, a.smem_bytes, a.err);
 }
 
-size_t greedy_smem_bytes(int M, int kalloc) { return greedy_layout(M, kalloc).bytes; }
+size_t greedy_smem_bytes(int algo, int M, int kalloc) { (void)algo; return greedy_layout(M, kalloc).bytes; }
 
 int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
   // Shared-memory LS capacity: the solver's bound (greedy_kalloc), trimmed so
@@ -572,7 +644,7 @@ int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap) {
   return k;
 }
 
-size_t greedy_ls_doubles(int M) { return (size_t)ls_doubles(M, M) + (size_t)csne_gram_doubles(M); }
+size_t greedy_ls_doubles(int M) { return (size_t)cta_scratch_doubles(M); }
 
 template <int ALGO>
 static cudaError_t launch_t(const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream) {
@@ -610,15 +682,28 @@ int greedy_blocks_per_sm(int algo, int M, size_t smem) {
 // basis_t[c N + r] = basis[r N + c]: a dictionary column gathered at the mask
 // rows then reads ascending addresses of one column (~20 sectors per 32 rows
 // instead of 32)
-__global__ void transpose_basis_kernel(const double* __restrict__ basis, int N, double* __restrict__ bt) {
+// Also checks, entry by entry, whether the basis is the orthonormal DCT-II
+// synthesis matrix Psi[r][c] = s_c cos(pi c (2 r + 1) / (2 N)) (exact integer
+// range reduction of c (2 r + 1) mod 4 N, cospi): *notdct stays 0 iff every
+// entry agrees to 1e-15 (entries are <= sqrt(2/N); a closed-form host basis
+// differs by ~1e-16).  Only then may the CSNE Gram use the DCT closed form.
+__global__ void transpose_basis_kernel(const double* __restrict__ basis, int N, double* __restrict__ bt,
+                                       int* notdct) {
+  const double s0 = sqrt(1.0 / (double)N), s1 = sqrt(2.0 / (double)N);
+  bool bad = false;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < N * N; idx += gridDim.x * blockDim.x) {
     const int c = idx / N, r = idx - c * N;
-    bt[idx] = basis[(size_t)r * N + c];
+    const double v = basis[(size_t)r * N + c];
+    bt[idx] = v;
+    const int q = (c * (2 * r + 1)) % (4 * N);
+    const double ref = (c ? s1 : s0) * cospi((double)q / (double)(2 * N));
+    bad |= !(fabs(v - ref) <= 1e-15);
   }
+  if (bad && notdct) atomicOr(notdct, 1);
 }
 
-cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, cudaStream_t stream) {
-  transpose_basis_kernel<<<64, 256, 0, stream>>>(basis, N, bt);
+cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, int* notdct, cudaStream_t stream) {
+  transpose_basis_kernel<<<64, 256, 0, stream>>>(basis, N, bt, notdct);
   return cudaGetLastError();
 }
 
@@ -644,7 +729,7 @@ extern "C" int hcs_debug_phases(unsigned long long* out16, int reset) {
 // the greedy kernel would use for (algo, M, kappa)
 extern "C" int hcs_debug_greedy_config(int algo, int M, int kappa, long long* out3) {
   const int k = hcs::greedy_kalloc_host(algo, M, kappa, 200 * 1024);
-  const size_t smem = hcs::greedy_smem_bytes(M, k);
+  const size_t smem = hcs::greedy_smem_bytes(algo, M, k);
   out3[0] = k;
   out3[1] = (long long)smem;
   out3[2] = hcs::greedy_blocks_per_sm(algo, M, smem);

@@ -54,6 +54,9 @@ struct GreedyArgs {
   unsigned smem_bytes = 0;   // dynamic shared bytes of the layout (checked builds: poison / canary)
   long long slots = 0;       // CTA scratch slots in gscratch
   int selftest = 0;          // checked builds: 1 = deliberately overrun the shared region (positive control)
+  // *notdct == 0: the basis is the orthonormal DCT-II (checked by transpose_basis_kernel), so the CSNE
+  // Gram takes the closed form of hcs_ls_csne.cuh (DctGram); nullptr: never
+  const int* notdct = nullptr;
 };
 
 // spill list of the warp-per-pixel gOMP kernel
@@ -77,10 +80,10 @@ cudaError_t launch_prep_basis(const double* basis, int N, int Np, double* fragS,
                               int slots, cudaStream_t stream);
 // hcs_greedy.cu
 cudaError_t launch_greedy(int algo, const GreedyArgs& args, int grid, size_t smem, cudaStream_t stream);
-size_t greedy_smem_bytes(int M, int kalloc);
+size_t greedy_smem_bytes(int algo, int M, int kalloc);
 int greedy_kalloc_host(int algo, int M, int kappa, size_t smem_cap);
 size_t greedy_ls_doubles(int M);
-cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, cudaStream_t stream);
+cudaError_t launch_transpose_basis(const double* basis, int N, double* bt, int* notdct, cudaStream_t stream);
 int greedy_blocks_per_sm(int algo, int M, size_t smem);
 // hcs_gomp_warp.cu
 bool gomp_warp_supported(int N, int M, int kappa);

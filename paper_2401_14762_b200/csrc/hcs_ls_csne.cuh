@@ -65,6 +65,30 @@ __device__ __forceinline__ int tri_row(int t) {
   return a;
 }
 
+// Gram entries of a DCT-II dictionary without touching its rows.  With
+// Psi[m][c] = s_c cos(theta_m c), theta_m = pi (2 m + 1) / (2 N), s_0 = sqrt(1/N),
+// s_c = sqrt(2/N), the product-to-sum identity gives, for A = Psi[mask, :],
+//     (A^T A)[i][j] = s_i s_j / 2 (F(|i - j|) + F(i + j)),
+//     F(d) = sum_{m in mask} cos(theta_m d),  F(N) = 0,  F(d) = -F(2 N - d) for d > N:
+// every Gram entry of every support is two lookups in the pixel's F (N
+// doubles, computed once per pixel as (A^T 1)[d] / s_d) instead of an M-term
+// dot product.  Used only when the basis was verified to be the DCT-II
+// (transpose_basis_kernel); any other orthonormal basis takes the DMMA Gram.
+struct DctGram {
+  const double* F;       // F(d), d < N (shared memory)
+  const double* q;       // A^T y over all N atoms (shared memory): the Gram's y row is q[cols[.]]
+  const uint8_t* cols;   // the system's dictionary column indices
+  int N;
+  double s0, s1;         // sqrt(1/N), sqrt(2/N)
+  double yty;            // y^T y
+};
+__device__ __forceinline__ double dct_gram_entry(const DctGram& dg, int ci, int cj) {
+  const int dm = ci > cj ? ci - cj : cj - ci, dp = ci + cj;
+  const double fm = dg.F[dm];
+  const double fp = dp < dg.N ? dg.F[dp] : (dp == dg.N ? 0.0 : -dg.F[2 * dg.N - dp]);
+  return (0.5 * (ci ? dg.s1 : dg.s0) * (cj ? dg.s1 : dg.s0)) * (fm + fp);
+}
+
 struct CsneScratch {   // shared memory
   double* G;      // csne_gram_doubles(K)
   double* dinv;   // >= round8(K + 1): 1 / L_ii
@@ -191,7 +215,7 @@ static __device__ __noinline__ void csne_diag_factor(double* G, const CsneScratc
   double rii = row[0];
 #pragma unroll
   for (int k = 1; k < 8; ++k) rii = (k == ii) ? row[k] : rii;
-  const double dii = (ii < w) ? 1.0 / rii : 0.0;
+  const double dii = (ii < w) ? __drcp_rn(rii) : 0.0;   // correctly rounded, as 1.0 / rii, off the DDIV path
   if (lane < 8) {
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -230,8 +254,10 @@ static __device__ __noinline__ void csne_diag_factor(double* G, const CsneScratc
 
 // Solve min ||B s - y|| (layout above).  Returns 1 with s[0..K) on success, 0
 // when a guard trips.  All threads call; ends synchronised.
+// DCT = true: `dg` supplies the closed-form augmented Gram (no dictionary column is read for it).
+template <bool DCT = false>
 static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K, double* s, const CsneScratch& sc,
-                              long long* ph = nullptr) {
+                              long long* ph = nullptr, const DctGram* dg = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
   const int M4 = (M + 3) & ~3;
   const int nbA = csne_cols(K) >> 3;      // block rows incl. the y row
@@ -247,6 +273,25 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
   auto gram_tile = [&](int t) {
     const int bi = tri_row(t);
     const int bj = t - bi * (bi + 1) / 2;
+    if (DCT && dg != nullptr) {
+      // the DCT-II closed form for atom x atom entries; row / column K of the
+      // augmented Gram is A^T y at the system's atoms, (K, K) is y^T y, the
+      // padding beyond K is zero: no dictionary column is read
+      const int i = lane >> 2, j0 = 2 * (lane & 3);
+      const int r = 8 * bi + i;
+      const int base = gtile(bi, bj) + i;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * bj + j0 + h;
+        double v = 0.0;
+        if (r < K && c < K) v = dct_gram_entry(*dg, dg->cols[r], dg->cols[c]);
+        else if (r == K && c == K) v = dg->yty;
+        else if (r == K && c < K) v = dg->q[dg->cols[c]];
+        else if (c == K && r < K) v = dg->q[dg->cols[r]];
+        G[base + (j0 + h) * 8] = v;
+      }
+      return;
+    }
     const double* ca = B + (8 * bi + (lane >> 2)) * ld + (lane & 3);
     const double* cb = B + (8 * bj + (lane >> 2)) * ld + (lane & 3);
     double d0[2] = {0.0, 0.0}, d1[2] = {0.0, 0.0};

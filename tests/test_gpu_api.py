@@ -390,3 +390,68 @@ def test_fista_kstep_skip_bitwise(monkeypatch, algo, lam):
         outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.final_delta, b.converged, b.admm_gap)])
     for u, v in zip(*outs):
         assert np.array_equal(u, v, equal_nan=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo,kappa", [("cosamp", 27), ("cosamp", 33), ("cosamp", 12)])
+def test_dct_closed_form_gram_matches_the_dmma_gram(monkeypatch, algo, kappa):
+    """CoSaMP least squares on wide systems: for a DCT-II basis the augmented
+    CSNE Gram comes from the product-to-sum closed form (hcs_ls_csne.cuh:
+    DctGram) instead of M-term DMMA dot products over the gathered columns.
+    Same significant supports, iterations and flags (but for roundoff-level
+    ties of the prune), coefficients within the refinement's accuracy of the
+    DMMA-Gram solve."""
+    import torch
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    c = synth.generate(8, 50, 224, seed=45)
+    dev = torch.device("cuda")
+    args = (torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev),
+            torch.as_tensor(c.basis, device=dev), SolverConfig(kappa=kappa, time_limit=None, max_iter=2000))
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HCS_DCT_GRAM", flag)
+        b = solve_batch(algo, *args)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.converged, b.failed_at)])
+    (x0, it0, cv0, f0), (x1, it1, cv1, f1) = outs
+    same = it0 == it1
+    assert same.mean() >= 0.97 and np.array_equal(cv0[same], cv1[same]) and np.array_equal(f0, f1)
+    nr = np.maximum(np.linalg.norm(x0[same], axis=1), 1e-300)
+    assert np.array_equal(np.abs(x0[same]) > 1e-9 * nr[:, None], np.abs(x1[same]) > 1e-9 * nr[:, None])
+    assert np.max(np.linalg.norm(x0[same] - x1[same], axis=1) / nr) < 1e-10
+
+
+@pytest.mark.gpu
+def test_non_dct_basis_takes_the_dmma_gram():
+    """A rotated (non-DCT) orthonormal basis must be detected on the device
+    (transpose_basis_kernel) and solved with the general Gram: CoSaMP and BIHT
+    against the oracle, and the workspace header word says 'not DCT'."""
+    import torch
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    n, m, P = 96, 40, 200
+    rng = np.random.default_rng(7)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    basis = np.ascontiguousarray(q)
+    x0 = np.zeros((P, n))
+    for p in range(P):
+        x0[p, rng.choice(n, size=6, replace=False)] = rng.uniform(0.5, 1.5, 6) * rng.choice([-1, 1], 6)
+    masks = np.sort(np.argsort(rng.random((P, n)), axis=1)[:, :m], axis=1).astype(np.uint8)
+    spectra = x0 @ basis.T
+    y = np.ascontiguousarray(np.take_along_axis(spectra, masks.astype(np.intp), axis=1))
+    dev = torch.device("cuda")
+    for algo, kappa in (("cosamp", 8), ("biht", 10)):
+        b = solve_batch(algo, torch.as_tensor(y, device=dev), torch.as_tensor(masks, device=dev),
+                        torch.as_tensor(basis, device=dev), SolverConfig(kappa=kappa, time_limit=None, max_iter=200))
+        torch.cuda.synchronize()
+        assert int(b.workspace[32:36].view(torch.int32).item()) == 1
+        ref = oc.solve_cube(algo, basis, y, masks, oc.OracleConfig(kappa=kappa, max_iter=200))
+        same = b.iterations.cpu().numpy() == ref.iterations
+        assert same.mean() >= 0.97
+        nr = np.maximum(np.linalg.norm(ref.x[same], axis=1), 1e-300)
+        assert np.max(np.linalg.norm(b.x.cpu().numpy()[same] - ref.x[same], axis=1) / nr) < 1e-9
+    # and the DCT basis itself is recognised
+    c = synth.generate(2, 50, 224, seed=3)
+    b = solve_batch("biht", torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev),
+                    torch.as_tensor(c.basis, device=dev), SolverConfig(kappa=27, time_limit=None, max_iter=50))
+    torch.cuda.synchronize()
+    assert int(b.workspace[32:36].view(torch.int32).item()) == 0

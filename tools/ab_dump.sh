@@ -23,5 +23,13 @@ for c in cases:
     for l in libs[1:]:
         z = np.load(f"{out}/{l}_{c}")
         same = all(np.array_equal(ref[k], z[k]) for k in ref.files)
-        print(f"{c}: {l} vs {libs[0]} bitwise identical: {same}")
+        msg = f"{c}: {l} vs {libs[0]} bitwise identical: {same}"
+        if not same:
+            nr = np.maximum(np.linalg.norm(ref["x"], axis=1), 1e-300)
+            rel = np.linalg.norm(ref["x"] - z["x"], axis=1) / nr
+            itd = ref["iterations"] != z["iterations"]
+            msg += (f"; iteration mismatches {int(itd.sum())}, converged mismatches "
+                    f"{int((ref['converged'] != z['converged']).sum())}, max rel dx over equal-iteration pixels "
+                    f"{rel[~itd].max():.2e}, pixels with rel dx > 1e-9: {int((rel[~itd] > 1e-9).sum())}")
+        print(msg)
 PY

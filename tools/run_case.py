@@ -67,6 +67,8 @@ def main():
                 print(f"  sparse GEMM: {ph[6] / ph[7]:.3f} of the dense 4 x 8 blocks active, masked path on "
                       f"{ph[8] / max(ph[9], 1):.3f} of the ticks")
             nit = max(int(it.sum()), 1)
+            print(f"  CTA cycles per pixel: {tot / cube.n_pixels:.0f} = " + ", ".join(
+                f"{nm} {ph[i] / cube.n_pixels:.0f}" for i, nm in enumerate(names)))
             print(f"  CTA cycles per pixel-iteration: {tot / nit:.0f} = " + ", ".join(
                 f"{nm} {ph[i] / nit:.0f}" for i, nm in enumerate(names)))
     if args.dump:
