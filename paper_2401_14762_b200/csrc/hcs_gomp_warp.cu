@@ -222,20 +222,21 @@ __device__ __forceinline__ double gw_norm(const double (&a)[MR], int lo) {
   return (n[0] + n[1]) + (n[2] + n[3]);
 }
 
-// the owner's column, rows >= 4 (j / 4), into vb
+// the owner's column, rows >= 16 (j / 16), into vb (gw_qr clears the rows below j)
 template <int MR>
 __device__ __forceinline__ void gw_copy(const double (&a)[MR], double* vb, int j) {
   double2* v2 = reinterpret_cast<double2*>(vb);
-  switch (j >> 2) {
-#define GW_CPY_CASE(k) case k: gw_copy_chunk<MR, k>(a, v2);
-    GW_CASES(GW_CPY_CASE)
+  switch (j >> 4) {
+#define GW_CPY_CASE(g) case g: gw_copy_chunk<MR, 4 * g>(a, v2); gw_copy_chunk<MR, 4 * g + 1>(a, v2); \
+                               gw_copy_chunk<MR, 4 * g + 2>(a, v2); gw_copy_chunk<MR, 4 * g + 3>(a, v2);
+    GW_GROUPS(GW_CPY_CASE)
 #undef GW_CPY_CASE
     default: break;
   }
 }
 
-// the owner's rows 0 .. 4 ceil(c / 4) - 1 into cb (R's column c above the
-// diagonal, plus rows >= c that the reader ignores): reverse Duff
+// the owner's rows 0 .. 16 ceil(c / 16) - 1 into cb (R's column c above the
+// diagonal, plus rows >= c that the reader ignores): reverse Duff over 16-row groups
 template <int MR, int CB>
 __device__ __forceinline__ void gw_rcol_chunk(const double (&a)[MR], double2* c2) {
   if constexpr (4 * CB + 3 < MR) {
@@ -246,12 +247,10 @@ __device__ __forceinline__ void gw_rcol_chunk(const double (&a)[MR], double2* c2
 template <int MR>
 __device__ __forceinline__ void gw_rcol(const double (&a)[MR], double* cb, int c) {
   double2* c2 = reinterpret_cast<double2*>(cb);
-  switch ((c + 3) >> 2) {   // chunks (c+3)/4 - 1 .. 0
-#define GW_RC_CASE(k) case k + 1: gw_rcol_chunk<MR, k>(a, c2);
-    GW_RC_CASE(23) GW_RC_CASE(22) GW_RC_CASE(21) GW_RC_CASE(20) GW_RC_CASE(19) GW_RC_CASE(18) GW_RC_CASE(17)
-    GW_RC_CASE(16) GW_RC_CASE(15) GW_RC_CASE(14) GW_RC_CASE(13) GW_RC_CASE(12) GW_RC_CASE(11) GW_RC_CASE(10) GW_RC_CASE(9)
-    GW_RC_CASE(8) GW_RC_CASE(7) GW_RC_CASE(6) GW_RC_CASE(5) GW_RC_CASE(4) GW_RC_CASE(3) GW_RC_CASE(2) GW_RC_CASE(1)
-    GW_RC_CASE(0)
+  switch ((c + 15) >> 4) {   // 16-row groups (c+15)/16 - 1 .. 0
+#define GW_RC_CASE(g) case g + 1: gw_rcol_chunk<MR, 4 * g + 3>(a, c2); gw_rcol_chunk<MR, 4 * g + 2>(a, c2); \
+                                  gw_rcol_chunk<MR, 4 * g + 1>(a, c2); gw_rcol_chunk<MR, 4 * g>(a, c2);
+    GW_RC_CASE(5) GW_RC_CASE(4) GW_RC_CASE(3) GW_RC_CASE(2) GW_RC_CASE(1) GW_RC_CASE(0)
 #undef GW_RC_CASE
     default: break;
   }
@@ -320,13 +319,13 @@ __device__ __forceinline__ void gw_qr(double (&a)[MR], double& rdiag, double (&y
       }
       if (lane == 0) vb[j] = amb;
     } else {
-      // v: row j -> alpha - beta; rows j0 .. j-1 of its chunk (just copied: R
-      // entries of the owner) and the previous chunk (the last reflectors'
-      // v, complete once j enters a new chunk) -> 0, so that vb is zero on
-      // every row below j for the straight-line dot / update
-      const int j0 = j & ~3;
-      if (lane <= j - j0) vb[j0 + lane] = (j0 + lane == j) ? amb : 0.0;
-      if (j0 == j && j >= 4 && lane >= 28) vb[j - 32 + lane] = 0.0;   // rows j-4 .. j-1
+      // v: row j -> alpha - beta; the rows below j of its 16-row group (just
+      // copied: R entries of the owner) -> 0, and row j - 1 (the last
+      // reflector's alpha - beta, possibly in the group before) -> 0, so
+      // that vb is zero on every row below j for the group-wise dot / update
+      const int g0 = j & ~15;
+      if (lane <= j - g0) vb[g0 + lane] = (g0 + lane == j) ? amb : 0.0;
+      if (j > 0 && lane == 31) vb[j - 1] = 0.0;
     }
     __syncwarp();
     double py = 0.0;

@@ -32,6 +32,9 @@ __device__ unsigned long long g_phase[16];
 #endif
 
 constexpr int kGreedyThreads = 128;
+#ifndef HCS_SMEM_ARGS_ALL
+#define HCS_SMEM_ARGS_ALL 0   // experiments: BIHT / gOMP also pass ls_csne's argument block through shared memory
+#endif
 constexpr int kRing = 64;  // state hashes kept for cycle detection (periods 2..63)
 
 struct GreedyShared {
@@ -306,6 +309,11 @@ __global__ void __launch_bounds__(kGreedyThreads, 4) greedy_kernel(GreedyArgs a)
       __syncthreads();
       GMARK(3);
       solved = ls_csne<true>(B, ldb, M, K, sv, g.cs, php, dct_far ? &g.dg : nullptr);
+    } else if constexpr (HCS_SMEM_ARGS_ALL) {
+      if (tid == 0) g.cs = CsneScratch{G, S + L.dinv, S + L.cv, yv, g.red, lsflag};
+      __syncthreads();
+      GMARK(3);
+      solved = ls_csne<false>(B, ldb, M, K, sv, g.cs, php);
     } else {
       __syncthreads();
       GMARK(3);

@@ -270,26 +270,44 @@ static __device__ __noinline__ int ls_csne(const double* B, int ld, int M, int K
   // (flag[1], 1 on entry); warp 0 joins them when its factorisation is done.
   // Every tile is computed by the same instructions whichever warp takes it.
   const int ntiles = nbA * (nbA + 1) / 2;
+  // the closed form's arguments in registers (dg points to shared memory)
+  const bool closed = DCT && dg != nullptr;
+  const double* dF = closed ? dg->F : nullptr;
+  const double* dq = closed ? dg->q : nullptr;
+  const uint8_t* dcols = closed ? dg->cols : nullptr;
+  const int dN = closed ? dg->N : 0;
+  const double ds0 = closed ? dg->s0 : 0.0, ds1 = closed ? dg->s1 : 0.0, dyty = closed ? dg->yty : 0.0;
+  auto gentry = [&](int ci, int cj) -> double {   // dct_gram_entry on the register copies
+    const int dm = ci > cj ? ci - cj : cj - ci, dp = ci + cj;
+    const double fm = dF[dm];
+    const double fp = dp < dN ? dF[dp] : (dp == dN ? 0.0 : -dF[2 * dN - dp]);
+    return (0.5 * (ci ? ds1 : ds0) * (cj ? ds1 : ds0)) * (fm + fp);
+  };
   auto gram_tile = [&](int t) {
     const int bi = tri_row(t);
     const int bj = t - bi * (bi + 1) / 2;
-    if (DCT && dg != nullptr) {
+    if (closed) {
       // the DCT-II closed form for atom x atom entries; row / column K of the
       // augmented Gram is A^T y at the system's atoms, (K, K) is y^T y, the
       // padding beyond K is zero: no dictionary column is read
       const int i = lane >> 2, j0 = 2 * (lane & 3);
-      const int r = 8 * bi + i;
+      const int r = 8 * bi + i, c = 8 * bj + j0;
       const int base = gtile(bi, bj) + i;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 8 * bj + j0 + h;
-        double v = 0.0;
-        if (r < K && c < K) v = dct_gram_entry(*dg, dg->cols[r], dg->cols[c]);
-        else if (r == K && c == K) v = dg->yty;
-        else if (r == K && c < K) v = dg->q[dg->cols[c]];
-        else if (c == K && r < K) v = dg->q[dg->cols[r]];
-        G[base + (j0 + h) * 8] = v;
+      // atom indices first (three independent loads), then the lookups
+      const int ar = r < K ? dcols[r] : -1;
+      const int ac0 = c < K ? dcols[c] : -1, ac1 = c + 1 < K ? dcols[c + 1] : -1;
+      double v0 = 0.0, v1 = 0.0;
+      if (ar >= 0) {
+        if (ac0 >= 0) v0 = gentry(ar, ac0);
+        else if (c == K) v0 = dq[ar];
+        if (ac1 >= 0) v1 = gentry(ar, ac1);
+        else if (c + 1 == K) v1 = dq[ar];
+      } else if (r == K) {
+        v0 = ac0 >= 0 ? dq[ac0] : (c == K ? dyty : 0.0);
+        v1 = ac1 >= 0 ? dq[ac1] : (c + 1 == K ? dyty : 0.0);
       }
+      G[base + j0 * 8] = v0;
+      G[base + (j0 + 1) * 8] = v1;
       return;
     }
     const double* ca = B + (8 * bi + (lane >> 2)) * ld + (lane & 3);
