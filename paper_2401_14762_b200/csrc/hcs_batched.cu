@@ -486,3 +486,57 @@ extern "C" int hcs_debug_phases_ls(unsigned long long* out16, int reset) {
   return 1;
 #endif
 }
+
+// Self-check of ddiv_fast / soft_fast (hcs_common.cuh) against __ddiv_rn / soft
+// on n pseudo-random operand pairs per mode: mode 0 moderate exponents
+// (2^-12 .. 2^12), 1 the full exponent range incl. subnormals, infinities and
+// NaN, 2 soft-threshold operands (|v| near and above t).
+// out[0] = accepted (ok) quotients, out[1] = accepted quotients that differ
+// from __ddiv_rn (must be 0), out[2] = rejected (redone by the caller).
+namespace hcs {
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void divcheck_kernel(unsigned long long n, unsigned long long seed, int mode, unsigned long long* out) {
+  unsigned long long acc = 0, bad = 0, rej = 0;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < n;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long u = mix64(seed + 2 * k), v = mix64(seed + 2 * k + 1);
+    double a, b;
+    if (mode == 0) {
+      a = __longlong_as_double((long long)((u & 0x800fffffffffffffull) | ((1011ull + (u >> 52) % 25) << 52)));
+      b = __longlong_as_double((long long)((v & 0x800fffffffffffffull) | ((1011ull + (v >> 52) % 25) << 52)));
+    } else if (mode == 1) {
+      a = __longlong_as_double((long long)u);
+      b = __longlong_as_double((long long)v);
+    } else {
+      const double t = ldexp(1.0 + (double)(u & 0xffff) / 65536.0, (int)((u >> 16) % 21) - 10);
+      const double rel = ldexp((double)(v >> 12), -52 - (int)((v & 0xfff) % 40));   // |v| = t (1 + rel)
+      const double mag = t * (1.0 + rel);
+      bool ok = true;
+      const double f = soft_fast((v >> 11) & 1 ? -mag : mag, t, ok), g = soft((v >> 11) & 1 ? -mag : mag, t);
+      if (ok) { ++acc; bad += __double_as_longlong(f) != __double_as_longlong(g); } else ++rej;
+      continue;
+    }
+    bool ok = true;
+    const double q = ddiv_fast(a, b, ok), ref = __ddiv_rn(a, b);
+    if (ok) { ++acc; bad += __double_as_longlong(q) != __double_as_longlong(ref); } else ++rej;
+  }
+  atomicAdd(out + 0, acc);
+  atomicAdd(out + 1, bad);
+  atomicAdd(out + 2, rej);
+}
+}  // namespace hcs
+
+extern "C" int hcs_debug_divcheck(unsigned long long n, unsigned long long seed, int mode, unsigned long long* out3) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, 3 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  cudaMemset(d, 0, 3 * sizeof(unsigned long long));
+  hcs::divcheck_kernel<<<148 * 8, 256>>>(n, seed, mode, d);
+  cudaError_t e = cudaMemcpy(out3, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : 1;
+}

@@ -28,6 +28,7 @@
 #include "hcs_gemm.cuh"
 #include "hcs_internal.cuh"
 #include <cstdlib>
+#include <type_traits>
 
 namespace hcs {
 
@@ -61,6 +62,35 @@ __device__ __forceinline__ int slot_idx(int k, int s) {
 }
 
 __host__ __device__ __forceinline__ int stage_mask_bytes(int M) { return ((M + 7) & ~7) + 8; }
+
+// Row -> measurement map in thread order.  Thread (w, lane) of the engine owns
+// the accumulator elements acc[rb][cb][i] = (row 8 (rb0 + rb) + lane / 4,
+// slot 8 cb + 2 (lane % 4) + i); their 16 map entries (0xFF: row not measured)
+// are the 16 bytes at pos + 16 (32 w + lane), entry (2 cb + i) MAXRB + rb, so an
+// epilogue gets all of them with one 16-byte shared load per tick instead of a
+// dependent byte load per element.  pos_addr is the inverse of warp_rows /
+// warp_rows16 for element (row n, slot s); RB = Np / 8, W = engine warps.
+template <int SL>
+__device__ __forceinline__ int pos_addr(int RB, int W, int n, int s) {
+  constexpr int MAXRB = (SL == 32) ? 2 : 4;
+  const int g = n >> 3;
+  int w, rbl;
+  if constexpr (SL == 32) {
+    const int nd = RB > 16 ? RB - 16 : 0;
+    if (g < 2 * nd) { w = g >> 1; rbl = g & 1; } else { w = g - nd; rbl = 0; }
+  } else {
+    const int base = RB / W, extra = RB % W, cut = extra * (base + 1);
+    if (g < cut) { w = g / (base + 1); rbl = g - w * (base + 1); }
+    else { const int q = (g - cut) / base; w = extra + q; rbl = (g - cut) - q * base; }
+  }
+  const int ln = ((n & 7) << 2) + ((s & 7) >> 1);
+  return (((w << 5) + ln) << 4) + ((s >> 3) * 2 + (s & 1)) * MAXRB + rbl;
+}
+// entry e of the 16 map bytes a thread loaded as one uint4
+__device__ __forceinline__ int pos_entry(const uint4& pw, int e) {
+  const unsigned v = e < 4 ? pw.x : e < 8 ? pw.y : e < 12 ? pw.z : pw.w;
+  return (int)((v >> (8 * (e & 3))) & 0xFFu);
+}
 
 // Claim the slot's next pixel from the work queue and start copying its
 // measurements, mask row and (fista) Lipschitz constant into the slot's
@@ -114,10 +144,10 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
                             uint8_t* pos, double* sy, uint8_t* sm, int s) {
   const int lane = threadIdx.x & 31;
   const int M = a.M, N = a.N, Np = a.Np, Mm = stage_mask_bytes(M);
-  uint8_t* ps = pos + s * kMaxN;
+  const int RB = Np >> 3, W = blockDim.x >> 5;
   for (int n = lane; n < Np; n += 32) {
     bufA[slot_idx<SL>(n, s)] = 0.0;
-    if (ALGO == kFista) bufB[slot_idx<SL>(n, s)] = 0.0;   // z_0 = 0
+    bufB[slot_idx<SL>(n, s)] = 0.0;   // fista: z_0 = 0; admm: u'_0 = 0 (r_0 = y - u'_0[mask] = y)
   }
   for (;;) {
     cp_async_wait_all();
@@ -125,7 +155,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
     const long long pid = ss.npid[s];
     if (pid >= a.P) {
       if (lane == 0) ss.status[s] = kEmpty;
-      for (int b = lane; b < kMaxN; b += 32) ps[b] = 0xFF;
+      for (int n = lane; n < Np; n += 32) pos[pos_addr<SL>(RB, W, n, s)] = 0xFF;
       __syncwarp();
       return;
     }
@@ -133,7 +163,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
     for (int j = lane; j < M; j += 32) {
       const double v = sy[s * M + j];
       ys[s * M + j] = v;
-      r[s * M + j] = v;
+      if (ALGO == kFista) r[s * M + j] = v;
       nz |= (v != 0.0);
       bad |= !isfinite(v);
     }
@@ -175,12 +205,12 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
       prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       continue;
     }
-    for (int b = lane; b < kMaxN; b += 32) ps[b] = 0xFF;
+    for (int n = lane; n < Np; n += 32) pos[pos_addr<SL>(RB, W, n, s)] = 0xFF;
     __syncwarp();
     const uint8_t* mrow = sm + s * Mm + ss.moff[s];
     for (int j = lane; j < M; j += 32) {
       const int row = mrow[j];
-      ps[row] = (uint8_t)j;
+      pos[pos_addr<SL>(RB, W, row, s)] = (uint8_t)j;
       if (ALGO == kFista) bufA[slot_idx<SL>(row, s)] = -ys[s * M + j];
     }
     if (lane == 0) {
@@ -244,7 +274,9 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState<
 // (<= 128 registers).  SL = 16: two CTAs per SM of 8 warps, up to 4 row blocks
 // x 2 column blocks each; the two CTAs drift out of phase so that one's
 // epilogues and slot phase overlap the other's GEMMs on the DMMA pipe.
-template <int ALGO, int SL, int MAXT, int MINB>
+// RING: A fragments through the per-warp cp.async ring of hcs_gemm.cuh (32-slot
+// engine, when the ring fits in shared memory) instead of register prefetch.
+template <int ALGO, int SL, int MAXT, int MINB, int RING>
 __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   if (*(volatile const int*)a.err & kErrMask) return;   // invalid masks (validate_masks_kernel)
   constexpr int CB = SL / 8;                  // 8-column blocks
@@ -260,13 +292,21 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   double* bufA = reinterpret_cast<double*>(smraw);      // Np * SL: fista g / x_{k+1}, admm z - w
   double* bufB = bufA + Np * SL;                        // Np * SL: fista z, admm u'
   double* ys = bufB + Np * SL;                          // SL * M
-  double* r = ys + SL * M;                              // SL * M
-  double* partD = r + SL * M;                           // 16 * SL residual-delta partials
-  double* partG = partD + 16 * SL;                      // 16 * SL admm gap partials
-  double* sy = partG + 16 * SL;                         // SL * M staged next measurements
+  double* r = ys + SL * M;                              // SL * M (fista; admm's is y - u'[mask], in bufB)
+  double* partD = r + (ALGO == kFista ? SL * M : 0);    // 16 * SL residual-delta partials
+  double* partG = partD + 16 * SL;                      // 16 * SL admm gap partials (admm)
+  double* sy = partG + (ALGO == kAdmm ? 16 * SL : 0);   // SL * M staged next measurements
   SlotState<SL>& ss = *reinterpret_cast<SlotState<SL>*>(sy + SL * M);
-  uint8_t* pos = reinterpret_cast<uint8_t*>(&ss + 1);   // SL * 256: row -> measurement index
+  // SL * 256: row -> measurement index in thread order (pos_addr), 16-byte aligned
+  uint8_t* pos = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(&ss + 1) + 15) & ~(uintptr_t)15);
   uint8_t* sm = pos + SL * kMaxN;                       // SL * stage_mask_bytes(M) staged mask rows
+  // this lane's slot in stage 0 of the warp's A-fragment ring (shared-space byte address)
+  unsigned ring = 0;
+  if constexpr (RING) {
+    unsigned char* rg = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(sm + SL * stage_mask_bytes(M)) + 15) & ~(uintptr_t)15);
+    ring = static_cast<unsigned>(__cvta_generic_to_shared(rg + ring_offset(Np >> 3, w))) + lane * 8 * nrb;
+  }
   const int cred = (SL == 32) ? col_of_reduced(lane) : col_of_reduced4(lane);
   const bool use_kskip = (SL == 32) && ALGO == kFista && a.kskip;
 
@@ -296,11 +336,23 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   double2 af[4];
   double af16[4][4];
   auto preload = [&](const double* m) {
-    if constexpr (SL == 32) gemm_preload(nrb, m, rb0, KS, af); else gemm_preload16(nrb, m, rb0, KS, af16);
+    if constexpr (RING) {
+      if (nrb == 2) ring_preload<2>(m, rb0, KS, ring); else ring_preload<1>(m, rb0, KS, ring);
+    } else if constexpr (SL == 32) {
+      gemm_preload(nrb, m, rb0, KS, af);
+    } else {
+      gemm_preload16(nrb, m, rb0, KS, af16);
+    }
   };
   double acc[MAXRB][CB][2];
   auto gemm = [&](const double* m, const double* in) {
-    if constexpr (SL == 32) tile_gemm(nrb, m, rb0, in, KS, acc, af); else tile_gemm16(nrb, m, rb0, in, KS, acc, af16);
+    if constexpr (RING) {
+      if (nrb == 2) tile_gemm_ring<2>(m, rb0, in, KS, acc, ring); else tile_gemm_ring<1>(m, rb0, in, KS, acc, ring);
+    } else if constexpr (SL == 32) {
+      tile_gemm(nrb, m, rb0, in, KS, acc, af);
+    } else {
+      tile_gemm16(nrb, m, rb0, in, KS, acc, af16);
+    }
   };
   auto reduce = [&](const double (&v)[NV]) -> double {
     if constexpr (SL == 32) return col_reduce8(v, lane); else return col_reduce4(v, lane);
@@ -314,6 +366,11 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #else
 #define CMARK(k) do {} while (0)
 #endif
+  // admm: 1 / (d + alpha) for d = 0, 1 (Psi orthonormal: the factor's eigenvalues);
+  // opaque to the optimiser, which otherwise rewrites x * (m ? inv1 : inv0) into
+  // a division per element
+  double inv0 = 1.0 / a.prm.alpha, inv1 = 1.0 / (1.0 + a.prm.alpha);
+  asm volatile("" : "+d"(inv0), "+d"(inv1));
   for (int tick = 0;; ++tick) {
     const int par = tick & 1;
     // ---- slot phase: stop rule of the last iteration, refill, momentum ----
@@ -401,33 +458,74 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 
     double part[NV];
     unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
+    // this thread's 16 row -> measurement entries (refills are done: barrier above)
+    const uint4 pw = *reinterpret_cast<const uint4*>(pos + 16 * threadIdx.x);
+    // The epilogues run per column block: all shared loads of the block's
+    // elements, then the arithmetic (independent chains the scheduler can
+    // interleave; the soft threshold's division on the branch-free path of
+    // soft_fast), then the stores.  NRB is the compile-time row-block count
+    // of the warp (exact for the 32-slot engine; the 16-slot engine passes
+    // its maximum and predicates on nrb).
     if (ALGO == kFista) {
       // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
       gemm(a.fragT, bufA);
       __syncthreads();
       CMARK(2);
+      auto epi1 = [&](auto nrbc) {
+        constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb)
+        for (int cb = 0; cb < CB; ++cb) {
+          double z[2][NRB], xn[2][NRB], il[2], th[2], bn[2];
+          int zi[2][NRB];
+          bool ok = true;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int s = acc_col(cb, i, lane);
-          const double il = ss.inv_l[s], th = ss.thr[s], bn = ss.betan[s];
-          bool bad = false;
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
+            il[i] = ss.inv_l[s];
+            th[i] = ss.thr[s];
+            bn[i] = ss.betan[s];
 #pragma unroll
-          for (int rb = 0; rb < MAXRB; ++rb) {
-            if (rb >= nrb) break;
-            const int zi = slot_idx<SL>(row0 + 8 * rb, s);
-            const double x = p0[rb][cb][i], z = bufB[zi];
-            const double aux = __dsub_rn(z, __dmul_rn(il, acc[rb][cb][i]));   // solvers.py:183
-            const double xn = soft(aux, th);                                    // solvers.py:185
-            bufB[zi] = __dadd_rn(xn, __dmul_rn(bn, __dsub_rn(xn, x)));         // solvers.py:189
-            p0[rb][cb][i] = xn;
-            bad |= !isfinite(xn);
-            bufA[zi] = xn;
-            if (xn != 0.0) kbits |= 1ull << ((row0 + 8 * rb) >> 2);
+            for (int rb = 0; rb < NRB; ++rb) {
+              zi[i][rb] = slot_idx<SL>(row0 + 8 * rb, s);
+              z[i][rb] = (rb < nrb) ? bufB[zi[i][rb]] : 0.0;
+            }
           }
-          if (bad) ss.flag[s] = 1;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              const double aux = __dsub_rn(z[i][rb], __dmul_rn(il[i], acc[rb][cb][i]));   // solvers.py:183
+              xn[i][rb] = soft_fast(aux, th[i], ok);                                       // solvers.py:185
+            }
+          if (!ok) {   // operands outside the fast division's range: the plain soft()
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int rb = 0; rb < NRB; ++rb)
+                xn[i][rb] = soft(__dsub_rn(z[i][rb], __dmul_rn(il[i], acc[rb][cb][i])), th[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            bool bad = false;
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              if (rb >= nrb) continue;
+              const double x = p0[rb][cb][i], v = xn[i][rb];
+              bufB[zi[i][rb]] = __dadd_rn(v, __dmul_rn(bn[i], __dsub_rn(v, x)));          // solvers.py:189
+              p0[rb][cb][i] = v;
+              bad |= !isfinite(v);
+              bufA[zi[i][rb]] = v;
+              if (v != 0.0) kbits |= 1ull << ((row0 + 8 * rb) >> 2);
+            }
+            if (bad) ss.flag[acc_col(cb, i, lane)] = 1;
+          }
         }
+      };
+      if constexpr (SL == 32) {
+        if (nrb == 2) epi1(std::integral_constant<int, 2>{}); else epi1(std::integral_constant<int, 1>{});
+      } else {
+        epi1(std::integral_constant<int, MAXRB>{});
+      }
       if (use_kskip) {
         const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits);
         const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits >> 32));
@@ -446,68 +544,116 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       __syncthreads();
       CMARK(4);
+      auto epi2 = [&](auto nrbc) {
+        constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb)
+        for (int cb = 0; cb < CB; ++cb) {
+          double yv[2][NRB], ro[2][NRB], rn[2][NRB], bn[2];
+          int pj[2][NRB];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int s = acc_col(cb, i, lane);
-          const double bn = ss.betan[s];
-          double dd = 0.0;
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
+            bn[i] = ss.betan[s];
 #pragma unroll
-          for (int rb = 0; rb < MAXRB; ++rb) {
-            if (rb >= nrb) break;
-            const int n = row0 + 8 * rb;
-            const int pj = pos[s * kMaxN + n];
-            double g = 0.0;
-            if (pj != 0xFF) {   // measured row: r = y - A x (solvers.py:192-196)
-              const double rn = ys[s * M + pj] - acc[rb][cb][i];
-              const double ro = r[s * M + pj];
-              const double d = rn - ro;
-              dd += d * d;
-              r[s * M + pj] = rn;
-              // next gradient input A z - y = -(1 + b) r + b r_prev
-              g = (bn == 0.0) ? -rn : -(1.0 + bn) * rn + bn * ro;
+            for (int rb = 0; rb < NRB; ++rb) {
+              const int e = pos_entry(pw, (2 * cb + i) * MAXRB + rb);
+              pj[i][rb] = (rb < nrb && e != 0xFF) ? s * M + e : -1;
+              yv[i][rb] = pj[i][rb] >= 0 ? ys[pj[i][rb]] : 0.0;
+              ro[i][rb] = pj[i][rb] >= 0 ? r[pj[i][rb]] : 0.0;
             }
-            bufA[slot_idx<SL>(n, s)] = g;
           }
-          part[2 * cb + i] = dd;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double dd = 0.0;
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              rn[i][rb] = yv[i][rb] - acc[rb][cb][i];   // measured row: r = y - A x (solvers.py:192-196)
+              if (pj[i][rb] >= 0) {
+                const double d = rn[i][rb] - ro[i][rb];
+                dd += d * d;
+              }
+            }
+            part[2 * cb + i] = dd;
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              if (rb >= nrb) continue;
+              double g = 0.0;
+              if (pj[i][rb] >= 0) {
+                const double rnv = rn[i][rb], rov = ro[i][rb], bnv = bn[i];
+                r[pj[i][rb]] = rnv;
+                // next gradient input A z - y = -(1 + b) r + b r_prev
+                g = (bnv == 0.0) ? -rnv : -(1.0 + bnv) * rnv + bnv * rov;
+              }
+              bufA[slot_idx<SL>(row0 + 8 * rb, s)] = g;
+            }
+          }
         }
+      };
+      if constexpr (SL == 32) {
+        if (nrb == 2) epi2(std::integral_constant<int, 2>{}); else epi2(std::integral_constant<int, 1>{});
+      } else {
+        epi2(std::integral_constant<int, MAXRB>{});
+      }
       partD[w * SL + cred] = reduce(part);
       preload(mat1);   // next GEMM's first k-steps
       __syncthreads();
       CMARK(5);
     } else {
       // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
-      //      residual y - A x = y - u'[mask] of this iteration's x ----------
+      //      residual y - A x = y - u'[mask] of this iteration's x; the last
+      //      residual is y - (the u' this epilogue overwrites)[mask] ----------
       gemm(a.fragS, bufA);
       CMARK(2);
       const double alpha = a.prm.alpha;
-      // 1 / (d + alpha) for d = 0, 1 (Psi orthonormal: the factor's eigenvalues)
-      const double inv0 = 1.0 / alpha, inv1 = 1.0 / (1.0 + alpha);
+      auto epi1 = [&](auto nrbc) {
+        constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb)
+        for (int cb = 0; cb < CB; ++cb) {
+          double yh[2][NRB], upo[2][NRB], up[2][NRB];
+          int idx[2][NRB];
+          bool in_mask[2][NRB];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int s = acc_col(cb, i, lane);
-          double dd = 0.0;
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
 #pragma unroll
-          for (int rb = 0; rb < MAXRB; ++rb) {
-            if (rb >= nrb) break;
-            const int n = row0 + 8 * rb;
-            const int pj = pos[s * kMaxN + n];
-            const bool in_mask = pj != 0xFF;
-            const double yh = in_mask ? ys[s * M + pj] : 0.0;
-            const double up = (yh + alpha * acc[rb][cb][i]) * (in_mask ? inv1 : inv0);
-            bufB[slot_idx<SL>(n, s)] = up;
-            if (in_mask) {
-              const double rn = yh - up;
-              const double d = rn - r[s * M + pj];
-              dd += d * d;
-              r[s * M + pj] = rn;
+            for (int rb = 0; rb < NRB; ++rb) {
+              const int e = pos_entry(pw, (2 * cb + i) * MAXRB + rb);
+              in_mask[i][rb] = rb < nrb && e != 0xFF;
+              idx[i][rb] = slot_idx<SL>(row0 + 8 * rb, s);
+              yh[i][rb] = in_mask[i][rb] ? ys[s * M + e] : 0.0;
+              upo[i][rb] = (rb < nrb) ? bufB[idx[i][rb]] : 0.0;
             }
           }
-          part[2 * cb + i] = dd;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double dd = 0.0;
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              up[i][rb] = (yh[i][rb] + alpha * acc[rb][cb][i]) * (in_mask[i][rb] ? inv1 : inv0);
+              if (in_mask[i][rb]) {
+                const double rn = yh[i][rb] - up[i][rb];
+                const double d = rn - (yh[i][rb] - upo[i][rb]);
+                dd += d * d;
+              }
+            }
+            part[2 * cb + i] = dd;
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb)
+              if (rb < nrb) bufB[idx[i][rb]] = up[i][rb];
         }
+      };
+      if constexpr (SL == 32) {
+        if (nrb == 2) epi1(std::integral_constant<int, 2>{}); else epi1(std::integral_constant<int, 1>{});
+      } else {
+        epi1(std::integral_constant<int, MAXRB>{});
+      }
       partD[w * SL + cred] = reduce(part);
       preload(mat2);   // next GEMM's first k-steps
       __syncthreads();
@@ -515,35 +661,57 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       // ---- GEMM 2: x = Psi^T u'; epilogue: shrink, dual update, gap --------
       gemm(a.fragT, bufB);
       CMARK(4);
+      auto epi2 = [&](auto nrbc) {
+        constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
-      for (int cb = 0; cb < CB; ++cb)
+        for (int cb = 0; cb < CB; ++cb) {
+          double zn[2][NRB], th[2];
+          bool ok = true;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int s = acc_col(cb, i, lane);
-          const double th = ss.thr[s];
-          const bool act = ss.status[s] == kActive;
-          double* xo = a.x_out + ss.pid[s] * N;
-          bool bad = false;
-          double g2 = 0.0;
+          for (int i = 0; i < 2; ++i) {
+            th[i] = ss.thr[acc_col(cb, i, lane)];
 #pragma unroll
-          for (int rb = 0; rb < MAXRB; ++rb) {
-            if (rb >= nrb) break;
-            const int n = row0 + 8 * rb;
-            const double x = acc[rb][cb][i], wv = p1[rb][cb][i];
-            const double zn = soft(__dadd_rn(x, wv), th);                 // solvers.py:229
-            const double wn = __dsub_rn(__dadd_rn(wv, x), zn);            // solvers.py:231
-            // z is the returned iterate: stored every pass (L2-absorbed), so
-            // it needs no registers between passes
-            if (act && n < N) xo[n] = zn;
-            p1[rb][cb][i] = wn;
-            bufA[slot_idx<SL>(n, s)] = zn - wn;                           // next GEMM 1 input
-            const double dg = x - zn;
-            g2 += dg * dg;
-            bad |= !isfinite(zn);
+            for (int rb = 0; rb < NRB; ++rb)
+              zn[i][rb] = soft_fast(__dadd_rn(acc[rb][cb][i], p1[rb][cb][i]), th[i], ok);   // solvers.py:229
           }
-          part[2 * cb + i] = g2;
-          if (bad) ss.flag[s] = 1;
+          if (!ok) {   // operands outside the fast division's range: the plain soft()
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int rb = 0; rb < NRB; ++rb) zn[i][rb] = soft(__dadd_rn(acc[rb][cb][i], p1[rb][cb][i]), th[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
+            const bool act = ss.status[s] == kActive;
+            double* xo = a.x_out + ss.pid[s] * N;
+            bool bad = false;
+            double g2 = 0.0;
+#pragma unroll
+            for (int rb = 0; rb < NRB; ++rb) {
+              if (rb >= nrb) continue;
+              const int n = row0 + 8 * rb;
+              const double x = acc[rb][cb][i], wv = p1[rb][cb][i], z = zn[i][rb];
+              const double wn = __dsub_rn(__dadd_rn(wv, x), z);            // solvers.py:231
+              // z is the returned iterate: stored every pass (L2-absorbed), so
+              // it needs no registers between passes
+              if (act && n < N) xo[n] = z;
+              p1[rb][cb][i] = wn;
+              bufA[slot_idx<SL>(n, s)] = z - wn;                           // next GEMM 1 input
+              const double dg = x - z;
+              g2 += dg * dg;
+              bad |= !isfinite(z);
+            }
+            part[2 * cb + i] = g2;
+            if (bad) ss.flag[s] = 1;
+          }
         }
+      };
+      if constexpr (SL == 32) {
+        if (nrb == 2) epi2(std::integral_constant<int, 2>{}); else epi2(std::integral_constant<int, 1>{});
+      } else {
+        epi2(std::integral_constant<int, MAXRB>{});
+      }
       partG[w * SL + cred] = reduce(part);
       preload(mat1);   // next GEMM's first k-steps
       __syncthreads();
@@ -745,17 +913,30 @@ cudaError_t launch_admm_zero(const ConvexArgs& args, long long* plist, unsigned 
   return cudaGetLastError();
 }
 
-size_t convex_smem_bytes(int algo, int Np, int M, int slots) {
-  (void)algo;
+// without the A-fragment ring
+static size_t convex_smem_base(int algo, int Np, int M, int slots) {
   const size_t sl = (size_t)slots;
   size_t b = sizeof(double) * (size_t)Np * sl * 2;                   // bufA, bufB
-  b += sizeof(double) * sl * M * 2;                                  // ys, r
-  b += sizeof(double) * 2 * 16 * sl;                                 // partD, partG
+  b += sizeof(double) * sl * M * (algo == kFista ? 2 : 1);           // ys, r (fista)
+  b += sizeof(double) * 16 * sl * (algo == kAdmm ? 2 : 1);           // partD, partG (admm)
   b += sizeof(double) * sl * M;                                      // sy
   b += slots == 32 ? sizeof(SlotState<32>) : sizeof(SlotState<16>);
-  b += sl * kMaxN;                                                   // pos
+  b += 16 + sl * kMaxN;                                              // pos (16-byte aligned)
   b += sl * stage_mask_bytes(M);                                     // sm
   return (b + 15) & ~(size_t)15;
+}
+
+// the 32-slot engine takes the A-fragment ring when it fits beside the rest
+// (HCS_CONVEX_RING=0: register prefetch, for A/B runs)
+bool convex_ring(int algo, int Np, int M, int slots) {
+  if (slots != 32) return false;
+  if (const char* ov = getenv("HCS_CONVEX_RING")) if (atoi(ov) == 0) return false;
+  return convex_smem_base(algo, Np, M, slots) + 16 + ring_bytes(Np) + kSmemExtra <= (size_t)227 * 1024;
+}
+
+size_t convex_smem_bytes(int algo, int Np, int M, int slots) {
+  const size_t b = convex_smem_base(algo, Np, M, slots);
+  return convex_ring(algo, Np, M, slots) ? b + 16 + ring_bytes(Np) : b;
 }
 
 // Slot engine variant for (Np, M): 32 slots x one CTA per SM (default).  The
@@ -783,26 +964,30 @@ int convex_ctas_per_sm(int algo, int Np, int M, int slots) {
   return 2 * (convex_smem_bytes(algo, Np, M, 16) + 1024) <= 228 * 1024 ? 2 : 1;
 }
 
-template <int ALGO, int SL, int MAXT, int MINB>
+template <int ALGO, int SL, int MAXT, int MINB, int RING>
 static cudaError_t launch_convex_t(const ConvexArgs& args, int grid, size_t smem, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, SL, MAXT, MINB>,
+  cudaError_t e = cudaFuncSetAttribute(convex_kernel<ALGO, SL, MAXT, MINB, RING>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem + kSmemExtra));
   if (e != cudaSuccess) return e;
   const int warps = SL == 32 ? engine_warps(args.Np) : engine_warps16(args.Np);
   ConvexArgs ca = args;
   ca.smem_bytes = (unsigned)smem;
-  convex_kernel<ALGO, SL, MAXT, MINB><<<grid, 32 * warps, smem + kSmemExtra, stream>>>(ca);
+  convex_kernel<ALGO, SL, MAXT, MINB, RING><<<grid, 32 * warps, smem + kSmemExtra, stream>>>(ca);
   return cudaGetLastError();
 }
 
 cudaError_t launch_convex(int algo, const ConvexArgs& args, int slots, int grid, cudaStream_t stream) {
   const size_t smem = convex_smem_bytes(algo, args.Np, args.M, slots);
   if (slots == 32) {
-    if (algo == kFista) return launch_convex_t<kFista, 32, 512, 1>(args, grid, smem, stream);
-    return launch_convex_t<kAdmm, 32, 512, 1>(args, grid, smem, stream);
+    if (convex_ring(algo, args.Np, args.M, slots)) {
+      if (algo == kFista) return launch_convex_t<kFista, 32, 512, 1, 1>(args, grid, smem, stream);
+      return launch_convex_t<kAdmm, 32, 512, 1, 1>(args, grid, smem, stream);
+    }
+    if (algo == kFista) return launch_convex_t<kFista, 32, 512, 1, 0>(args, grid, smem, stream);
+    return launch_convex_t<kAdmm, 32, 512, 1, 0>(args, grid, smem, stream);
   }
-  if (algo == kFista) return launch_convex_t<kFista, 16, 256, 2>(args, grid, smem, stream);
-  return launch_convex_t<kAdmm, 16, 256, 2>(args, grid, smem, stream);
+  if (algo == kFista) return launch_convex_t<kFista, 16, 256, 2, 0>(args, grid, smem, stream);
+  return launch_convex_t<kAdmm, 16, 256, 2, 0>(args, grid, smem, stream);
 }
 
 }  // namespace hcs

@@ -180,6 +180,110 @@ __device__ __forceinline__ void tile_gemm(int nrb, const double* frag, int rb0, 
   if (nrb == 2) tile_gemm<2>(frag, rb0, In, KS, acc, a); else tile_gemm<1>(frag, rb0, In, KS, acc, a);
 }
 
+// ---------------------------------------------------------------------------
+// A fragments through a per-warp shared-memory ring (cp.async, kRing k-steps
+// deep).  With the fragments loaded straight into registers (tile_gemm) ptxas
+// puts every in-flight __ldg of the loop on one scoreboard, so the wait for the
+// oldest fragment also waits for the youngest: the 4-k-step prefetch distance
+// collapses to ~0 and a quarter of the GEMM's stall samples are long-scoreboard
+// waits (profiles/ncu_admm_ring_r02.txt).  cp.async groups are counted
+// (cp.async.wait_group kRing - 1 = DEPBAR.LE), so the ring really runs kRing - 1
+// k-steps ahead of the DMMAs.  Each lane copies and reads back only its own
+// 8 NRB bytes per k-step: no cross-lane synchronisation.  Stage st of a warp's
+// ring is at byte st * 256 * NRB; the warp's ring base is ring_offset().
+constexpr int kRing = 4;
+
+// bytes of all rings of a 32-slot CTA / byte offset of warp w's ring
+__host__ __device__ __forceinline__ int ring_bytes(int Np) {
+  const int RB = Np >> 3, W = RB < 16 ? RB : 16, nd = RB > 16 ? RB - 16 : 0;
+  return kRing * 256 * (2 * nd + (W - nd));
+}
+__device__ __forceinline__ int ring_offset(int RB, int w) {
+  const int nd = RB > 16 ? RB - 16 : 0;
+  return kRing * 256 * (w < nd ? 2 * w : nd + w);
+}
+
+template <int NRB>
+__device__ __forceinline__ void ring_copy(unsigned dst, const double* src) {
+  if (NRB == 2) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
+// the same copy, ordered after the register `dep` is available (the ring
+// stage's last read has landed before the stage is overwritten)
+template <int NRB>
+__device__ __forceinline__ void ring_copy_after(unsigned dst, const double* src, double dep) {
+  if (NRB == 2) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src), "d"(dep));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src), "d"(dep));
+}
+__device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void ring_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+template <int NRB>
+__device__ __forceinline__ double2 ring_read(unsigned src) {
+  double2 v;
+  if (NRB == 2) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(src));
+  } else {
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v.x) : "r"(src));
+    v.y = 0.0;
+  }
+  return v;
+}
+
+// first kRing k-steps of the next GEMM into the ring (issued before the barrier
+// that precedes the GEMM); ring = shared-space byte address of this lane's
+// slot in stage 0
+template <int NRB>
+__device__ __forceinline__ void ring_preload(const double* __restrict__ frag, int rb0, int KS, unsigned ring) {
+  const int lane = threadIdx.x & 31;
+  const double* src = frag + (size_t)rb0 * KS * 32 + lane * NRB;
+#pragma unroll
+  for (int st = 0; st < kRing; ++st) {
+    ring_copy<NRB>(ring + st * 256 * NRB, src + (size_t)st * 32 * NRB);
+    ring_commit();
+  }
+}
+
+// acc = Mat(row blocks rb0 .. rb0 + NRB - 1) * In with the A fragments from the
+// ring (ring_preload done).  KS is a multiple of 4 = kRing.  Same DMMA order
+// per accumulator as tile_gemm: bitwise-identical results.
+template <int NRB>
+__device__ __forceinline__ void tile_gemm_ring(const double* __restrict__ frag, int rb0, const double* In, int KS,
+                                               double (&acc)[2][4][2], unsigned ring) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int rb = 0; rb < NRB; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+  const double* src = frag + (size_t)rb0 * KS * 32 + lane * NRB;
+  ring_wait<kRing - 1>();
+  double2 a = ring_read<NRB>(ring);
+  for (int ks0 = 0; ks0 < KS; ks0 += kRing) {
+#pragma unroll
+    for (int i = 0; i < kRing; ++i) {
+      const int ks = ks0 + i;
+      const double* b = In + (ks << 7) + lane;
+      const double b0 = b[0], b1 = b[32], b2 = b[64], b3 = b[96];
+      dmma(acc[0][0], a.x, b0);
+      if (NRB == 2) dmma(acc[1][0], a.y, b0);
+      // stage i is in registers: refill it with k-step ks + kRing, then fetch
+      // the next k-step's fragment (complete once <= kRing - 1 groups pend)
+      if (ks + kRing < KS) ring_copy_after<NRB>(ring + i * 256 * NRB, src + (size_t)(ks + kRing) * 32 * NRB, a.x);
+      ring_commit();
+      ring_wait<kRing - 1>();
+      double2 an = a;
+      if (ks + 1 < KS) an = ring_read<NRB>(ring + ((i + 1) % kRing) * 256 * NRB);
+      dmma(acc[0][1], a.x, b1);
+      if (NRB == 2) dmma(acc[1][1], a.y, b1);
+      dmma(acc[0][2], a.x, b2);
+      if (NRB == 2) dmma(acc[1][2], a.y, b2);
+      dmma(acc[0][3], a.x, b3);
+      if (NRB == 2) dmma(acc[1][3], a.y, b3);
+      a = an;
+    }
+  }
+}
+
 // Column sums of an accumulator-layout quantity: v[2 cb + i] is this lane's
 // value for slot column 8 cb + 2 (lane & 3) + i (already summed over its row
 // blocks).  Three transpose-and-add butterfly stages over the 8 lanes sharing
