@@ -32,7 +32,9 @@
 
 namespace hcs {
 
-enum { kEmpty = 0, kActive = 1 };
+// slot states: kEmpty (to be refilled in the next slot phase), kActive, kDead
+// (queue exhausted: never refilled again)
+enum { kEmpty = 0, kActive = 1, kDead = 3 };
 
 #ifdef HCS_PHASES
 __device__ unsigned long long g_phase_cx[16];
@@ -49,9 +51,12 @@ struct SlotState {
   double inv_l[SL], thr[SL];
   int status[SL], iter[SL], flag[SL], rfail[SL], retired[SL], moff[SL], need_pf[SL];
   int nact[2];
+  // per tick parity: slots whose pixel retired / slots refilled or emptied in
+  // this tick's slot phase (their columns' iterates restart from zero)
+  unsigned retmask[2], freshmask[2];
   int exhausted;
   long long np;           // pixels in the queue (P, or *plist_n)
-  unsigned long long kmask;   // fista: k-steps of x_{k+1} with a nonzero in some slot
+  unsigned long long kmask[2];   // fista, per tick parity: k-steps of x_{k+1} with a nonzero in some slot
 };
 
 // Slot-column layout of the GEMM input buffers: 32 slots (one CTA per SM) or 16
@@ -154,7 +159,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
     __syncwarp();
     const long long pid = ss.npid[s];
     if (pid >= a.P) {
-      if (lane == 0) ss.status[s] = kEmpty;
+      if (lane == 0) ss.status[s] = kDead;
       for (int n = lane; n < Np; n += 32) pos[pos_addr<SL>(RB, W, n, s)] = 0xFF;
       __syncwarp();
       return;
@@ -325,10 +330,17 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   if (threadIdx.x == 0) {
     ss.exhausted = 0;
     ss.nact[0] = ss.nact[1] = 0;
+    ss.retmask[0] = ss.retmask[1] = ss.freshmask[0] = ss.freshmask[1] = 0u;
+    ss.kmask[0] = ss.kmask[1] = 0ull;
     ss.np = a.plist ? (long long)*a.plist_n : a.P;
   }
   __syncthreads();
-  for (int s = w; s < SL; s += W) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
+  // Slot owners: warp w handles slots w + W k.  (Giving all slots to the four
+  // one-block warps, which have half a GEMM of slack, measured 12% slower: under
+  // the other warps' DMMAs their serial slot code runs ~6x longer than the slack.)
+  const int nown = W, ow = w;
+  if (ow >= 0)
+    for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
   const double* mat1 = (ALGO == kFista) ? a.fragT : a.fragS;
   const double* mat2 = (ALGO == kFista) ? a.fragS : a.fragT;
@@ -374,12 +386,22 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   for (int tick = 0;; ++tick) {
     const int par = tick & 1;
     // ---- slot phase: stop rule of the last iteration, refill, momentum ----
+    // Runs inside the GEMM 1 window (no barrier between it and the GEMM): each
+    // warp handles its own slots, then joins the GEMM, which runs optimistically
+    // on every column.  The column of a slot that retires or is refilled here
+    // is garbage in this GEMM (the refill rewrites it underneath); the
+    // epilogues after the barrier replace it: admm takes the product of the
+    // fresh pixel's zero input (exactly 0) and a zero dual, so the new pixel's
+    // first iteration still runs in this tick.  fista needs Psi^T g of the new
+    // g = -y: it keeps a barrier between the slot phase and the GEMM (letting a
+    // fresh column sit one tick out instead measured 2.4% slower).
     // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
     // serial stop-rule / momentum code of a warp's slots runs side by side
-    for (int s0 = w; s0 < SL; s0 += 2 * W) {
-      const int hl = lane & 15, s = s0 + (lane >> 4) * W;
+    for (int s0 = ow >= 0 ? ow : SL; s0 < SL; s0 += 2 * nown) {
+      const int hl = lane & 15, s = s0 + (lane >> 4) * nown;
       const bool valid = s < SL;
-      const bool was_active = valid && ss.status[s] == kActive;
+      const int st0 = valid ? ss.status[s] : kDead;
+      const bool was_active = st0 == kActive;
       double dd = (was_active && hl < W) ? partD[hl * SL + s] : 0.0;
       double gg = (ALGO == kAdmm && was_active && hl < W) ? partG[hl * SL + s] : 0.0;
 #pragma unroll
@@ -392,19 +414,24 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (was_active) {
           if (ALGO == kFista) ss.t[s] = ss.tn[s];
           finish_iteration<SL>(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
+          if (ss.retired[s]) atomicOr(&ss.retmask[par], 1u << s);
         }
       }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        const int sk = s0 + k * W;
+        const int sk = s0 + k * nown;
         if (sk >= SL) break;
         if (ALGO == kAdmm && ss.retired[sk] && ss.rfail[sk])   // NumericalFailure: x = 0
           for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
-        if (ss.status[sk] != kActive) refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+        if (ss.status[sk] == kEmpty) {
+          refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+          if (lane == 0) atomicOr(&ss.freshmask[par], 1u << sk);
+        }
       }
       if (hl == 0 && valid) {
-        if (ss.status[s] == kActive) {
+        const int st1 = ss.status[s];
+        if (st1 == kActive) {
           atomicAdd(&ss.nact[par], 1);
           ss.flag[s] = 0;
           if (ALGO == kFista) {
@@ -421,40 +448,67 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       __syncwarp();
     }
-    if (threadIdx.x == 0) {
-      ss.nact[par ^ 1] = 0;
-      ss.kmask = 0ull;
-    }
-    __syncthreads();
     CMARK(0);
-    for (int s = w; s < SL; s += W)
+    for (int s = ow >= 0 ? ow : SL; s < SL; s += nown)
       if (ss.need_pf[s]) {
         __syncwarp();
         if (lane == 0) ss.need_pf[s] = 0;
         prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       }
-
-    // ---- writeback of retired slots (element layout), fresh iterates -------
-#pragma unroll
-    for (int cb = 0; cb < CB; ++cb)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int s = acc_col(cb, i, lane);
-        if (ss.retired[s]) {
-          const long long pid = ss.rpid[s];
-          const bool fail = ss.rfail[s];
-#pragma unroll
-          for (int rb = 0; rb < MAXRB; ++rb) {
-            if (rb >= nrb) break;
-            const int n = row0 + 8 * rb;
-            if (ALGO == kFista && n < N) a.x_out[pid * N + n] = fail ? 0.0 : p0[rb][cb][i];
-            p0[rb][cb][i] = 0.0;
-            p1[rb][cb][i] = 0.0;
-          }
-        }
+    // masks of this tick's slot phase, read after the barrier that follows it
+    // (fista: the one before GEMM 1, whose input the refills wrote; admm: the
+    // one after GEMM 1)
+    unsigned retm = 0u, freshm = 0u;
+    bool done = false;
+    auto read_masks = [&]() {
+      retm = ss.retmask[par];
+      freshm = ss.freshmask[par];
+      done = ss.nact[par] == 0;
+      if (threadIdx.x == 0) {
+        ss.nact[par ^ 1] = 0;
+        ss.retmask[par ^ 1] = 0u;
+        ss.freshmask[par ^ 1] = 0u;
+        ss.kmask[par ^ 1] = 0ull;
       }
-    if (ss.nact[par] == 0) break;
+    };
+    if (ALGO == kFista) {
+      __syncthreads();
+      read_masks();
+      // result of the slots that retired (element layout); x_0 = 0 for the
+      // refilled / emptied ones
+      if (retm | freshm) {
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int s = acc_col(cb, i, lane);
+            if ((retm >> s) & 1u) {
+              const long long pid = ss.rpid[s];
+              const bool fail = ss.rfail[s];
+#pragma unroll
+              for (int rb = 0; rb < MAXRB; ++rb) {
+                if (rb >= nrb) break;
+                const int n = row0 + 8 * rb;
+                if (n < N) a.x_out[pid * N + n] = fail ? 0.0 : p0[rb][cb][i];
+              }
+            }
+            if ((freshm >> s) & 1u) {
+#pragma unroll
+              for (int rb = 0; rb < MAXRB; ++rb) p0[rb][cb][i] = 0.0;
+            }
+          }
+      }
+      if (done) break;
+    }
     CMARK(1);
+    // ---- GEMM 1 (fista: grad = Psi^T g; admm: v = Psi (z - w)) ------------
+    gemm(mat1, bufA);
+    __syncthreads();   // (admm: slot phase and) GEMM 1 of every warp done
+    CMARK(2);
+    if (ALGO == kAdmm) {
+      read_masks();
+      if (done) break;
+    }
 
     double part[NV];
     unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
@@ -467,10 +521,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     // of the warp (exact for the 32-slot engine; the 16-slot engine passes
     // its maximum and predicates on nrb).
     if (ALGO == kFista) {
-      // ---- GEMM 1: grad = Psi^T g; epilogue: prox-gradient + momentum -----
-      gemm(a.fragT, bufA);
-      __syncthreads();
-      CMARK(2);
+      // ---- epilogue 1: prox-gradient + momentum ---------------------------
       auto epi1 = [&](auto nrbc) {
         constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
@@ -490,19 +541,20 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
               z[i][rb] = (rb < nrb) ? bufB[zi[i][rb]] : 0.0;
             }
           }
+          // (skipping the divisions of a block that shrinks to zero as a whole,
+          // behind a warp vote, measured 2.6% slower)
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
-              const double aux = __dsub_rn(z[i][rb], __dmul_rn(il[i], acc[rb][cb][i]));   // solvers.py:183
-              xn[i][rb] = soft_fast(aux, th[i], ok);                                       // solvers.py:185
+              z[i][rb] = __dsub_rn(z[i][rb], __dmul_rn(il[i], acc[rb][cb][i]));   // aux, solvers.py:183
+              xn[i][rb] = soft_fast(z[i][rb], th[i], ok);                          // solvers.py:185
             }
           if (!ok) {   // operands outside the fast division's range: the plain soft()
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int rb = 0; rb < NRB; ++rb)
-                xn[i][rb] = soft(__dsub_rn(z[i][rb], __dmul_rn(il[i], acc[rb][cb][i])), th[i]);
+              for (int rb = 0; rb < NRB; ++rb) xn[i][rb] = soft(z[i][rb], th[i]);
           }
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
@@ -529,7 +581,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       if (use_kskip) {
         const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)kbits);
         const unsigned hi = __reduce_or_sync(0xffffffffu, (unsigned)(kbits >> 32));
-        if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask, ((unsigned long long)hi << 32) | lo);
+        if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask[par], ((unsigned long long)hi << 32) | lo);
       }
       preload(mat2);   // next GEMM's first k-steps (the dense path's)
       __syncthreads();
@@ -537,8 +589,8 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
       // the masked loop only when at most half the k-steps are active (it
       // prefetches 2 steps ahead instead of 4: slower on a dense mask)
-      if (use_kskip && 2 * __popcll(ss.kmask) <= KS) {
-        if constexpr (SL == 32) tile_gemm_masked(nrb, a.fragS, rb0, bufA, KS, ss.kmask, acc);
+      if (use_kskip && 2 * __popcll(ss.kmask[par]) <= KS) {
+        if constexpr (SL == 32) tile_gemm_masked(nrb, a.fragS, rb0, bufA, KS, ss.kmask[par], acc);
       } else {
         gemm(a.fragS, bufA);
       }
@@ -606,8 +658,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
       //      residual y - A x = y - u'[mask] of this iteration's x; the last
       //      residual is y - (the u' this epilogue overwrites)[mask] ----------
-      gemm(a.fragS, bufA);
-      CMARK(2);
       const double alpha = a.prm.alpha;
       auto epi1 = [&](auto nrbc) {
         constexpr int NRB = decltype(nrbc)::value;
@@ -633,7 +683,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             double dd = 0.0;
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
-              up[i][rb] = (yh[i][rb] + alpha * acc[rb][cb][i]) * (in_mask[i][rb] ? inv1 : inv0);
+              // a slot refilled in this tick: Psi times its zero input
+              const double v = ((freshm >> acc_col(cb, i, lane)) & 1u) ? 0.0 : acc[rb][cb][i];
+              up[i][rb] = (yh[i][rb] + alpha * v) * (in_mask[i][rb] ? inv1 : inv0);
               if (in_mask[i][rb]) {
                 const double rn = yh[i][rb] - up[i][rb];
                 const double d = rn - (yh[i][rb] - upo[i][rb]);
@@ -670,6 +722,10 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             th[i] = ss.thr[acc_col(cb, i, lane)];
+            if ((freshm >> acc_col(cb, i, lane)) & 1u) {   // refilled / emptied: w_0 = 0
+#pragma unroll
+              for (int rb = 0; rb < NRB; ++rb) p1[rb][cb][i] = 0.0;
+            }
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb)
               zn[i][rb] = soft_fast(__dadd_rn(acc[rb][cb][i], p1[rb][cb][i]), th[i], ok);   // solvers.py:229

@@ -60,3 +60,24 @@ def test_cta_topk_matches_argmax_k(n):
             want = tuple(int(i) for i in oc.argmax_k(v[row], k))
             assert got[row] == want, (n, k, row)
             assert old[row] == want, (n, k, row)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_fast_division_is_ddiv_rn(mode):
+    """The branch-free division of the convex epilogues (ddiv_fast / soft_fast,
+    hcs_common.cuh) against __ddiv_rn / soft on 2^28 operand pairs: every
+    quotient it accepts is bit-identical; pairs outside its range are rejected
+    (redone with __ddiv_rn by the caller).  Modes: moderate exponents, the full
+    bit range (subnormals, infinities, NaN), soft-threshold operands."""
+    lib = _native.load()
+    lib.hcs_debug_divcheck.argtypes = [ctypes.c_ulonglong, ctypes.c_ulonglong, ctypes.c_int,
+                                       ctypes.POINTER(ctypes.c_ulonglong)]
+    out = (ctypes.c_ulonglong * 3)()
+    assert lib.hcs_debug_divcheck(1 << 28, 777 + mode, mode, out) == 0
+    accepted, different, rejected = out[0], out[1], out[2]
+    assert accepted + rejected == 1 << 28
+    assert different == 0
+    if mode != 1:
+        assert rejected == 0          # ordinary operands always take the fast path
+    else:
+        assert accepted > (1 << 27)   # and most of the full bit range too

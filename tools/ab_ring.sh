@@ -22,4 +22,4 @@ for f in sorted(glob.glob(out + "/head_*.npz")):
         print(c, l, "bitwise identical:", all(same.values()), {k: v for k, v in same.items() if not v})
 PY
 rm -f $out/*.npz
-for r in 0 1; do echo "== bench-size, HCS_CONVEX_RING=$r"; HCS_CONVEX_RING=$r bash tools/ab_bench_convex.sh paper_2401_14762_b200/libhypercs_b200.so; done
+for r in 1; do echo "== bench-size, HCS_CONVEX_RING=$r"; HCS_CONVEX_RING=$r bash tools/ab_bench_convex.sh paper_2401_14762_b200/libhypercs_b200.so; done
