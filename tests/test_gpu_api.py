@@ -393,6 +393,31 @@ def test_fista_kstep_skip_bitwise(monkeypatch, algo, lam):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("algo,lam,n", [("fista", 0.1, 224), ("admm", 0.1, 224), ("admm", 3.0, 224),
+                                        ("fista", 0.1, 198), ("admm", 1.0, 154)])
+def test_ring_and_register_fragment_paths_bitwise(monkeypatch, algo, lam, n):
+    """The slot engine's A fragments through the per-warp cp.async ring
+    (default when it fits in shared memory) against the register-prefetch GEMM
+    (HCS_CONVEX_RING=0): the same DMMA order per accumulator, so every output
+    is bit-for-bit the same; enough pixels that slots retire and refill."""
+    import torch
+    from paper_2401_14762_b200.solvers import SolverConfig, solve_batch
+    c = synth.generate(30, 170, n, seed=45)   # 5100 px: > 148 x 32 slots, so slots refill
+    dev = torch.device("cuda")
+    args = (torch.as_tensor(c.y, device=dev), torch.as_tensor(c.masks, device=dev), torch.as_tensor(c.basis, device=dev),
+            SolverConfig(lam=lam, time_limit=None, max_iter=400))
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HCS_CONVEX_RING", flag)
+        b = solve_batch(algo, *args)
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (b.x, b.iterations, b.final_delta, b.converged, b.admm_gap)])
+    assert outs[0][1].max() > 1
+    for u, v in zip(*outs):
+        assert np.array_equal(u, v, equal_nan=True)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("algo,kappa", [("cosamp", 27), ("cosamp", 33), ("cosamp", 12)])
 def test_dct_closed_form_gram_matches_the_dmma_gram(monkeypatch, algo, kappa):
     """CoSaMP least squares on wide systems: for a DCT-II basis the augmented
