@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
               rn[i][rb] = yv[i][rb] - acc[rb][cb][i];   // measured row: r = y - A x (solvers.py:192-196)
               if (pj[i][rb] >= 0) {
                 const double d = rn[i][rb] - ro[i][rb];
-                dd += d * d;
+                dd = fma(d, d, dd);
               }
             }
             part[2 * cb + i] = dd;
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
               if (in_mask[i][rb]) {
                 const double rn = yh[i][rb] - up[i][rb];
                 const double d = rn - (yh[i][rb] - upo[i][rb]);
-                dd += d * d;
+                dd = fma(d, d, dd);
               }
             }
             part[2 * cb + i] = dd;
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
               p1[rb][cb][i] = wn;
               bufA[slot_idx<SL>(n, s)] = z - wn;                           // next GEMM 1 input
               const double dg = x - z;
-              g2 += dg * dg;
+              g2 = fma(dg, dg, g2);
               bad |= !isfinite(z);
             }
             part[2 * cb + i] = g2;
@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(256) admm_zero_kernel(ConvexArgs a, long long*
         if (ms[k]) {
           const double rn = yh[k] - up;
           const double d = rn - rp[k];
-          dd += d * d;
+          dd = fma(d, d, dd);
           rp[k] = rn;
         }
         const double xw = up + W[k];
