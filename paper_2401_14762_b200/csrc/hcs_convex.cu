@@ -339,8 +339,18 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   // one-block warps, which have half a GEMM of slack, measured 12% slower: under
   // the other warps' DMMAs their serial slot code runs ~6x longer than the slack.)
   const int nown = W, ow = w;
-  if (ow >= 0)
+  // fista (slot phase between two barriers): one warp owns every slot, one lane
+  // per slot: 2% faster than two slots per warp (931 against 950 ms at bench
+  // size); admm (slot phase under the other warps' GEMM): no gain (1491 against
+  // 1485 ms), it keeps two slots per warp
+  constexpr bool kSlotWarp = ALGO == kFista;
+  const bool slot_warp = w == W - 1;
+  if constexpr (kSlotWarp) {
+    if (slot_warp)
+      for (int s = 0; s < SL; ++s) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
+  } else {
     for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
+  }
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
   const double* mat1 = (ALGO == kFista) ? a.fragT : a.fragS;
   const double* mat2 = (ALGO == kFista) ? a.fragS : a.fragT;
@@ -395,6 +405,81 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     // first iteration still runs in this tick.  fista needs Psi^T g of the new
     // g = -y: it keeps a barrier between the slot phase and the GEMM (letting a
     // fresh column sit one tick out instead measured 2.4% slower).
+    if constexpr (kSlotWarp) {
+    // one warp, one lane per slot: the partial sums in the tree order of the
+    // half-warp version, masks and the active count by ballots (no atomics)
+    if (slot_warp) {
+      const int sl_ = lane;
+      const bool valid = sl_ < SL;
+      const int st0 = valid ? ss.status[sl_] : kDead;
+      const bool was_active = st0 == kActive;
+      double pd[16], pg[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        pd[i] = (was_active && i < W) ? partD[i * SL + sl_] : 0.0;
+        pg[i] = (ALGO == kAdmm && was_active && i < W) ? partG[i * SL + sl_] : 0.0;
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+          pd[i] += pd[i + o];
+          if (ALGO == kAdmm) pg[i] += pg[i + o];
+        }
+      if (valid) {
+        ss.retired[sl_] = 0;
+        if (was_active) {
+          if (ALGO == kFista) ss.t[sl_] = ss.tn[sl_];
+          finish_iteration<SL>(a, ss, sl_, sqrt(pd[0]), ALGO == kAdmm, pg[0]);
+        }
+      }
+      __syncwarp();
+      const unsigned retb = __ballot_sync(0xffffffffu, valid && ss.retired[sl_]);
+      unsigned failb = (ALGO == kAdmm) ? __ballot_sync(0xffffffffu, valid && ss.retired[sl_] && ss.rfail[sl_]) : 0u;
+      while (failb) {   // NumericalFailure: x = 0
+        const int sk = __ffs(failb) - 1;
+        failb &= failb - 1;
+        for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
+      }
+      const unsigned emptyb = __ballot_sync(0xffffffffu, valid && ss.status[sl_] == kEmpty);
+      for (unsigned em = emptyb; em;) {
+        const int sk = __ffs(em) - 1;
+        em &= em - 1;
+        refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+      }
+      __syncwarp();
+      const int st1 = valid ? ss.status[sl_] : kDead;
+      if (valid) {
+        if (st1 == kActive) {
+          ss.flag[sl_] = 0;
+          if (ALGO == kFista) {
+            const double t = ss.t[sl_];
+            const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));   // solvers.py:160-161
+            ss.tn[sl_] = tn;
+            ss.betan[sl_] = (t - 1.0) / tn;
+          }
+        } else {
+          ss.inv_l[sl_] = 0.0;
+          ss.thr[sl_] = 0.0;
+          ss.betan[sl_] = 0.0;
+        }
+      }
+      const unsigned actb = __ballot_sync(0xffffffffu, st1 == kActive);
+      if (lane == 0) {
+        ss.nact[par] = __popc(actb);
+        ss.retmask[par] = retb;
+        ss.freshmask[par] = emptyb;
+      }
+      __syncwarp();
+      CMARK(0);
+      for (unsigned pf = __ballot_sync(0xffffffffu, valid && ss.need_pf[sl_]); pf;) {
+        const int sk = __ffs(pf) - 1;
+        pf &= pf - 1;
+        if (lane == 0) ss.need_pf[sk] = 0;
+        prefetch_slot<ALGO, SL>(a, ss, sy, sm, sk);
+      }
+    }
+    } else {
     // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
     // serial stop-rule / momentum code of a warp's slots runs side by side
     for (int s0 = ow >= 0 ? ow : SL; s0 < SL; s0 += 2 * nown) {
@@ -455,6 +540,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (lane == 0) ss.need_pf[s] = 0;
         prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       }
+    }
     // masks of this tick's slot phase, read after the barrier that follows it
     // (fista: the one before GEMM 1, whose input the refills wrote; admm: the
     // one after GEMM 1)
