@@ -39,6 +39,13 @@ enum { kEmpty = 0, kActive = 1, kDead = 3 };
 #ifdef HCS_PHASES
 __device__ unsigned long long g_phase_cx[16];
 #endif
+// debug builds (-DHCS_TRACE): per-warp clock64 at the marks of ticks 200..203 of CTA 0
+#ifdef HCS_TRACE
+__device__ long long g_trace[4][16][12];
+#define TMARK(k) do { if (blockIdx.x == 0 && tick >= 200 && tick < 204 && lane == 0) g_trace[tick - 200][w][k] = clock64(); } while (0)
+#else
+#define TMARK(k) do {} while (0)
+#endif
 
 template <int SL>
 struct SlotState {
@@ -294,10 +301,15 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   int rb0, nrb;
   if constexpr (SL == 32) warp_rows(Np >> 3, w, rb0, nrb); else warp_rows16(Np >> 3, W, w, rb0, nrb);
   const int row0 = 8 * rb0 + (lane >> 2);   // element row of acc[rb] is row0 + 8 rb
+  // buffer index of this thread's element acc[rb][cb][i]: one base plus
+  // compile-time offsets (slot_idx of row row0 + 8 rb, slot 8 cb + 2 (lane & 3) + i)
+  const int ebase = slot_idx<SL>(row0, 2 * (lane & 3));
+  auto eidx = [&](int rb, int cb, int i) { return ebase + rb * (2 * (SL / 8) * 32) + cb * 32 + i * 4; };
   double* bufA = reinterpret_cast<double*>(smraw);      // Np * SL: fista g / x_{k+1}, admm z - w
   double* bufB = bufA + Np * SL;                        // Np * SL: fista z, admm u'
   double* ys = bufB + Np * SL;                          // SL * M
   double* r = ys + SL * M;                              // SL * M (fista; admm's is y - u'[mask], in bufB)
+  const double* ysq = ys + 2 * (lane & 3) * M;          // measurements of slot 2 (lane & 3); slot 8 cb + i: (8 cb + i) M further
   double* partD = r + (ALGO == kFista ? SL * M : 0);    // 16 * SL residual-delta partials
   double* partG = partD + 16 * SL;                      // 16 * SL admm gap partials (admm)
   double* sy = partG + (ALGO == kAdmm ? 16 * SL : 0);   // SL * M staged next measurements
@@ -395,6 +407,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   asm volatile("" : "+d"(inv0), "+d"(inv1));
   for (int tick = 0;; ++tick) {
     const int par = tick & 1;
+    TMARK(0);
     // ---- slot phase: stop rule of the last iteration, refill, momentum ----
     // Runs inside the GEMM 1 window (no barrier between it and the GEMM): each
     // warp handles its own slots, then joins the GEMM, which runs optimistically
@@ -587,9 +600,12 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       if (done) break;
     }
     CMARK(1);
+    TMARK(1);
     // ---- GEMM 1 (fista: grad = Psi^T g; admm: v = Psi (z - w)) ------------
     gemm(mat1, bufA);
+    TMARK(2);
     __syncthreads();   // (admm: slot phase and) GEMM 1 of every warp done
+    TMARK(3);
     CMARK(2);
     if (ALGO == kAdmm) {
       read_masks();
@@ -623,7 +639,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             bn[i] = ss.betan[s];
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
-              zi[i][rb] = slot_idx<SL>(row0 + 8 * rb, s);
+              zi[i][rb] = eidx(rb, cb, i);
               z[i][rb] = (rb < nrb) ? bufB[zi[i][rb]] : 0.0;
             }
           }
@@ -670,7 +686,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (lane == 0 && (lo | hi)) atomicOr(&ss.kmask[par], ((unsigned long long)hi << 32) | lo);
       }
       preload(mat2);   // next GEMM's first k-steps (the dense path's)
+      TMARK(4);
       __syncthreads();
+      TMARK(5);
       CMARK(3);
       // ---- GEMM 2: F = Psi x_{k+1}; epilogue: residual, delta, next g -------
       // the masked loop only when at most half the k-steps are active (it
@@ -680,7 +698,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       } else {
         gemm(a.fragS, bufA);
       }
+      TMARK(6);
       __syncthreads();
+      TMARK(7);
       CMARK(4);
       auto epi2 = [&](auto nrbc) {
         constexpr int NRB = decltype(nrbc)::value;
@@ -695,7 +715,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
               const int e = pos_entry(pw, (2 * cb + i) * MAXRB + rb);
-              pj[i][rb] = (rb < nrb && e != 0xFF) ? s * M + e : -1;
+              pj[i][rb] = (rb < nrb && e != 0xFF) ? (2 * (lane & 3) + 8 * cb + i) * M + e : -1;
               yv[i][rb] = pj[i][rb] >= 0 ? ys[pj[i][rb]] : 0.0;
               ro[i][rb] = pj[i][rb] >= 0 ? r[pj[i][rb]] : 0.0;
             }
@@ -726,7 +746,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
                 // next gradient input A z - y = -(1 + b) r + b r_prev
                 g = (bnv == 0.0) ? -rnv : -(1.0 + bnv) * rnv + bnv * rov;
               }
-              bufA[slot_idx<SL>(row0 + 8 * rb, s)] = g;
+              bufA[eidx(rb, cb, i)] = g;
             }
           }
         }
@@ -738,13 +758,25 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       partD[w * SL + cred] = reduce(part);
       preload(mat1);   // next GEMM's first k-steps
+      TMARK(8);
       __syncthreads();
+      TMARK(9);
       CMARK(5);
     } else {
       // ---- GEMM 1: v = Psi (z - w); epilogue: u' = (yhat + alpha v) / (d + alpha),
       //      residual y - A x = y - u'[mask] of this iteration's x; the last
       //      residual is y - (the u' this epilogue overwrites)[mask] ----------
       const double alpha = a.prm.alpha;
+      if (freshm) {   // slots refilled in this tick: Psi times their zero input, and a zero dual
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            if ((freshm >> acc_col(cb, i, lane)) & 1u) {
+#pragma unroll
+              for (int rb = 0; rb < MAXRB; ++rb) acc[rb][cb][i] = p1[rb][cb][i] = 0.0;
+            }
+      }
       auto epi1 = [&](auto nrbc) {
         constexpr int NRB = decltype(nrbc)::value;
 #pragma unroll
@@ -759,8 +791,8 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             for (int rb = 0; rb < NRB; ++rb) {
               const int e = pos_entry(pw, (2 * cb + i) * MAXRB + rb);
               in_mask[i][rb] = rb < nrb && e != 0xFF;
-              idx[i][rb] = slot_idx<SL>(row0 + 8 * rb, s);
-              yh[i][rb] = in_mask[i][rb] ? ys[s * M + e] : 0.0;
+              idx[i][rb] = eidx(rb, cb, i);
+              yh[i][rb] = in_mask[i][rb] ? ysq[(8 * cb + i) * M + e] : 0.0;
               upo[i][rb] = (rb < nrb) ? bufB[idx[i][rb]] : 0.0;
             }
           }
@@ -769,9 +801,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             double dd = 0.0;
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
-              // a slot refilled in this tick: Psi times its zero input
-              const double v = ((freshm >> acc_col(cb, i, lane)) & 1u) ? 0.0 : acc[rb][cb][i];
-              up[i][rb] = (yh[i][rb] + alpha * v) * (in_mask[i][rb] ? inv1 : inv0);
+              up[i][rb] = (yh[i][rb] + alpha * acc[rb][cb][i]) * (in_mask[i][rb] ? inv1 : inv0);
               if (in_mask[i][rb]) {
                 const double rn = yh[i][rb] - up[i][rb];
                 const double d = rn - (yh[i][rb] - upo[i][rb]);
@@ -794,10 +824,14 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       partD[w * SL + cred] = reduce(part);
       preload(mat2);   // next GEMM's first k-steps
+      TMARK(4);
       __syncthreads();
+      TMARK(5);
       CMARK(3);
       // ---- GEMM 2: x = Psi^T u'; epilogue: shrink, dual update, gap --------
       gemm(a.fragT, bufB);
+      TMARK(6);
+      TMARK(7);
       CMARK(4);
       auto epi2 = [&](auto nrbc) {
         constexpr int NRB = decltype(nrbc)::value;
@@ -808,10 +842,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             th[i] = ss.thr[acc_col(cb, i, lane)];
-            if ((freshm >> acc_col(cb, i, lane)) & 1u) {   // refilled / emptied: w_0 = 0
-#pragma unroll
-              for (int rb = 0; rb < NRB; ++rb) p1[rb][cb][i] = 0.0;
-            }
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb)
               zn[i][rb] = soft_fast(__dadd_rn(acc[rb][cb][i], p1[rb][cb][i]), th[i], ok);   // solvers.py:229
@@ -839,7 +869,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
               // it needs no registers between passes
               if (act && n < N) xo[n] = z;
               p1[rb][cb][i] = wn;
-              bufA[slot_idx<SL>(n, s)] = z - wn;                           // next GEMM 1 input
+              bufA[eidx(rb, cb, i)] = z - wn;                              // next GEMM 1 input
               const double dg = x - z;
               g2 = fma(dg, dg, g2);
               bad |= !isfinite(z);
@@ -856,7 +886,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       }
       partG[w * SL + cred] = reduce(part);
       preload(mat1);   // next GEMM's first k-steps
+      TMARK(8);
       __syncthreads();
+      TMARK(9);
       CMARK(5);
     }
   }
@@ -1133,6 +1165,16 @@ cudaError_t launch_convex(int algo, const ConvexArgs& args, int slots, int grid,
 }
 
 }  // namespace hcs
+
+// debug builds (-DHCS_TRACE): the per-warp tick timeline of CTA 0 (4 ticks x 16 warps x 12 marks)
+extern "C" int hcs_debug_trace_cx(long long* out768) {
+#ifdef HCS_TRACE
+  return cudaMemcpyFromSymbol(out768, hcs::g_trace, sizeof(long long) * 4 * 16 * 12) == cudaSuccess ? 0 : 2;
+#else
+  (void)out768;
+  return 1;
+#endif
+}
 
 // debug builds: per-phase cycle totals of the convex kernel (summed over CTAs)
 extern "C" int hcs_debug_phases_cx(unsigned long long* out16, int reset) {
