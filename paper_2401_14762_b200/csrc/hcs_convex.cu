@@ -34,7 +34,16 @@ namespace hcs {
 
 // slot states: kEmpty (to be refilled in the next slot phase), kActive, kDead
 // (queue exhausted: never refilled again)
-enum { kEmpty = 0, kActive = 1, kDead = 3 };
+enum { kEmpty = 0, kActive = 1, kFresh = 2, kDead = 3 };
+// fista with the slot phase inside the GEMM-1 window (no barrier before the
+// GEMM): a refilled slot is kFresh for the rest of its tick (its columns are
+// skipped by the epilogues; GEMM 1 needs Psi^T of its new g = -y) and starts
+// in the next tick
+#ifdef HCS_FISTA_OVERLAP
+constexpr bool kFistaOverlap = true;
+#else
+constexpr bool kFistaOverlap = false;
+#endif
 
 #ifdef HCS_PHASES
 __device__ unsigned long long g_phase_cx[16];
@@ -228,7 +237,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
     if (lane == 0) {
       ss.pid[s] = pid;
       ss.start[s] = t0;
-      ss.status[s] = kActive;
+      ss.status[s] = (ALGO == kFista && kFistaOverlap) ? kFresh : kActive;
       ss.iter[s] = 0;
       ss.t[s] = 1.0;
       if (ALGO == kFista) {
@@ -444,6 +453,8 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (was_active) {
           if (ALGO == kFista) ss.t[sl_] = ss.tn[sl_];
           finish_iteration<SL>(a, ss, sl_, sqrt(pd[0]), ALGO == kAdmm, pg[0]);
+        } else if (st0 == kFresh) {   // staged in the last tick: starts now
+          ss.status[sl_] = kActive;
         }
       }
       __syncwarp();
@@ -471,13 +482,13 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             ss.tn[sl_] = tn;
             ss.betan[sl_] = (t - 1.0) / tn;
           }
-        } else {
+        } else if (st1 != kFresh) {
           ss.inv_l[sl_] = 0.0;
           ss.thr[sl_] = 0.0;
           ss.betan[sl_] = 0.0;
         }
       }
-      const unsigned actb = __ballot_sync(0xffffffffu, st1 == kActive);
+      const unsigned actb = __ballot_sync(0xffffffffu, st1 == kActive || st1 == kFresh);
       if (lane == 0) {
         ss.nact[par] = __popc(actb);
         ss.retmask[par] = retb;
@@ -570,9 +581,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         ss.kmask[par ^ 1] = 0ull;
       }
     };
-    if (ALGO == kFista) {
-      __syncthreads();
-      read_masks();
+    auto fista_results = [&]() {
       // result of the slots that retired (element layout); x_0 = 0 for the
       // refilled / emptied ones
       if (retm | freshm) {
@@ -597,6 +606,11 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             }
           }
       }
+    };
+    if (ALGO == kFista && !kFistaOverlap) {
+      __syncthreads();
+      read_masks();
+      fista_results();
       if (done) break;
     }
     CMARK(1);
@@ -611,6 +625,13 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       read_masks();
       if (done) break;
     }
+    if (ALGO == kFista && kFistaOverlap) {
+      read_masks();
+      fista_results();
+      if (done) break;
+    }
+    // fista overlap: columns refilled in this tick sit it out
+    const unsigned skipm = (ALGO == kFista && kFistaOverlap) ? freshm : 0u;
 
     double part[NV];
     unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
@@ -661,6 +682,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             bool bad = false;
+            if ((skipm >> acc_col(cb, i, lane)) & 1u) continue;
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
               if (rb >= nrb) continue;
@@ -736,6 +758,10 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int s = acc_col(cb, i, lane);
+            if ((skipm >> s) & 1u) {   // the refilled g = -y and r = y stay
+              part[2 * cb + i] = 0.0;
+              continue;
+            }
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
               if (rb >= nrb) continue;
