@@ -34,16 +34,7 @@ namespace hcs {
 
 // slot states: kEmpty (to be refilled in the next slot phase), kActive, kDead
 // (queue exhausted: never refilled again)
-enum { kEmpty = 0, kActive = 1, kFresh = 2, kDead = 3 };
-// fista with the slot phase inside the GEMM-1 window (no barrier before the
-// GEMM): a refilled slot is kFresh for the rest of its tick (its columns are
-// skipped by the epilogues; GEMM 1 needs Psi^T of its new g = -y) and starts
-// in the next tick
-#ifdef HCS_FISTA_OVERLAP
-constexpr bool kFistaOverlap = true;
-#else
-constexpr bool kFistaOverlap = false;
-#endif
+enum { kEmpty = 0, kActive = 1, kDead = 3 };
 
 #ifdef HCS_PHASES
 __device__ unsigned long long g_phase_cx[16];
@@ -237,7 +228,7 @@ __device__ void refill_slot(const ConvexArgs& a, SlotState<SL>& ss, double* bufA
     if (lane == 0) {
       ss.pid[s] = pid;
       ss.start[s] = t0;
-      ss.status[s] = (ALGO == kFista && kFistaOverlap) ? kFresh : kActive;
+      ss.status[s] = kActive;
       ss.iter[s] = 0;
       ss.t[s] = 1.0;
       if (ALGO == kFista) {
@@ -366,12 +357,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   // 1485 ms), it keeps two slots per warp
   constexpr bool kSlotWarp = ALGO == kFista;
   const bool slot_warp = w == W - 1;
-  if constexpr (kSlotWarp) {
-    if (slot_warp)
-      for (int s = 0; s < SL; ++s) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
-  } else {
-    for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
-  }
+  for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
   const double* mat1 = (ALGO == kFista) ? a.fragT : a.fragS;
   const double* mat2 = (ALGO == kFista) ? a.fragS : a.fragT;
@@ -453,8 +439,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (was_active) {
           if (ALGO == kFista) ss.t[sl_] = ss.tn[sl_];
           finish_iteration<SL>(a, ss, sl_, sqrt(pd[0]), ALGO == kAdmm, pg[0]);
-        } else if (st0 == kFresh) {   // staged in the last tick: starts now
-          ss.status[sl_] = kActive;
         }
       }
       __syncwarp();
@@ -465,15 +449,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         failb &= failb - 1;
         for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
       }
-      const unsigned emptyb = __ballot_sync(0xffffffffu, valid && ss.status[sl_] == kEmpty);
-      for (unsigned em = emptyb; em;) {
-        const int sk = __ffs(em) - 1;
-        em &= em - 1;
-        refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
-      }
-      __syncwarp();
       const int st1 = valid ? ss.status[sl_] : kDead;
-      if (valid) {
+      const unsigned emptyb = __ballot_sync(0xffffffffu, st1 == kEmpty);
+      if (valid && st1 != kEmpty) {
         if (st1 == kActive) {
           ss.flag[sl_] = 0;
           if (ALGO == kFista) {
@@ -482,27 +460,52 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
             ss.tn[sl_] = tn;
             ss.betan[sl_] = (t - 1.0) / tn;
           }
-        } else if (st1 != kFresh) {
+        } else {
           ss.inv_l[sl_] = 0.0;
           ss.thr[sl_] = 0.0;
           ss.betan[sl_] = 0.0;
         }
       }
-      const unsigned actb = __ballot_sync(0xffffffffu, st1 == kActive || st1 == kFresh);
+      const unsigned actb = __ballot_sync(0xffffffffu, st1 == kActive);
       if (lane == 0) {
-        ss.nact[par] = __popc(actb);
+        ss.nact[par] = __popc(actb);   // the refills below add theirs
         ss.retmask[par] = retb;
         ss.freshmask[par] = emptyb;
       }
-      __syncwarp();
-      CMARK(0);
-      for (unsigned pf = __ballot_sync(0xffffffffu, valid && ss.need_pf[sl_]); pf;) {
-        const int sk = __ffs(pf) - 1;
-        pf &= pf - 1;
-        if (lane == 0) ss.need_pf[sk] = 0;
-        prefetch_slot<ALGO, SL>(a, ss, sy, sm, sk);
-      }
     }
+    __syncthreads();
+    // refills by the slots' owner warps (w + W k: the warp that staged the next
+    // pixel), in parallel; the extra barrier only in ticks that refill
+    if (const unsigned em = ss.freshmask[par]) {
+      for (int sk = ow; sk < SL; sk += nown)
+        if ((em >> sk) & 1u) {
+          refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
+          if (lane == 0) {
+            if (ss.status[sk] == kActive) {
+              atomicAdd(&ss.nact[par], 1);
+              ss.flag[sk] = 0;
+              if (ALGO == kFista) {
+                const double t = ss.t[sk];
+                const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));   // solvers.py:160-161
+                ss.tn[sk] = tn;
+                ss.betan[sk] = (t - 1.0) / tn;
+              }
+            } else {
+              ss.inv_l[sk] = 0.0;
+              ss.thr[sk] = 0.0;
+              ss.betan[sk] = 0.0;
+            }
+          }
+        }
+      __syncthreads();
+    }
+    CMARK(0);
+    for (int s = ow; s < SL; s += nown)
+      if (ss.need_pf[s]) {
+        __syncwarp();
+        if (lane == 0) ss.need_pf[s] = 0;
+        prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
+      }
     } else {
     // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
     // serial stop-rule / momentum code of a warp's slots runs side by side
@@ -607,8 +610,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
           }
       }
     };
-    if (ALGO == kFista && !kFistaOverlap) {
-      __syncthreads();
+    if (ALGO == kFista) {
       read_masks();
       fista_results();
       if (done) break;
@@ -625,13 +627,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       read_masks();
       if (done) break;
     }
-    if (ALGO == kFista && kFistaOverlap) {
-      read_masks();
-      fista_results();
-      if (done) break;
-    }
-    // fista overlap: columns refilled in this tick sit it out
-    const unsigned skipm = (ALGO == kFista && kFistaOverlap) ? freshm : 0u;
 
     double part[NV];
     unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
@@ -682,7 +677,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             bool bad = false;
-            if ((skipm >> acc_col(cb, i, lane)) & 1u) continue;
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
               if (rb >= nrb) continue;
@@ -758,10 +752,6 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int s = acc_col(cb, i, lane);
-            if ((skipm >> s) & 1u) {   // the refilled g = -y and r = y stay
-              part[2 * cb + i] = 0.0;
-              continue;
-            }
 #pragma unroll
             for (int rb = 0; rb < NRB; ++rb) {
               if (rb >= nrb) continue;
