@@ -355,7 +355,11 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   // per slot: 2% faster than two slots per warp (931 against 950 ms at bench
   // size); admm (slot phase under the other warps' GEMM): no gain (1491 against
   // 1485 ms), it keeps two slots per warp
+#ifdef HCS_ADMM_SLOT_WARP
+  constexpr bool kSlotWarp = true;
+#else
   constexpr bool kSlotWarp = ALGO == kFista;
+#endif
   const bool slot_warp = w == W - 1;
   for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
@@ -615,15 +619,19 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       fista_results();
       if (done) break;
     }
+    if (ALGO == kAdmm && kSlotWarp) {
+      read_masks();
+      if (done) break;
+    }
     CMARK(1);
     TMARK(1);
     // ---- GEMM 1 (fista: grad = Psi^T g; admm: v = Psi (z - w)) ------------
     gemm(mat1, bufA);
     TMARK(2);
-    __syncthreads();   // (admm: slot phase and) GEMM 1 of every warp done
+    if (ALGO == kFista || !kSlotWarp) __syncthreads();   // (admm: slot phase and) GEMM 1 of every warp done
     TMARK(3);
     CMARK(2);
-    if (ALGO == kAdmm) {
+    if (ALGO == kAdmm && !kSlotWarp) {
       read_masks();
       if (done) break;
     }
