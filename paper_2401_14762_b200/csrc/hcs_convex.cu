@@ -347,19 +347,15 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
     ss.np = a.plist ? (long long)*a.plist_n : a.P;
   }
   __syncthreads();
-  // Slot owners: warp w handles slots w + W k.  (Giving all slots to the four
-  // one-block warps, which have half a GEMM of slack, measured 12% slower: under
-  // the other warps' DMMAs their serial slot code runs ~6x longer than the slack.)
+  // Slot phase: the stop rule (and fista's momentum) of all slots is run by one
+  // warp with one lane per slot; refills and the staging of the next pixel stay
+  // with the slot's owner warp, w + W k (cp.async completion is per thread).
+  // Measured alternatives (profiles/convex_ring_r02.txt): two slots per warp
+  // via half-warp shuffles (3.3k cycles per tick instead of 1.7k); all slot
+  // work including refills in one warp (serialises 32 refills per tick when
+  // pixels converge in one iteration); the slot phase under the other warps'
+  // GEMM (its code runs 6-8x longer under DMMA contention).
   const int nown = W, ow = w;
-  // fista (slot phase between two barriers): one warp owns every slot, one lane
-  // per slot: 2% faster than two slots per warp (931 against 950 ms at bench
-  // size); admm (slot phase under the other warps' GEMM): no gain (1491 against
-  // 1485 ms), it keeps two slots per warp
-#ifdef HCS_ADMM_SLOT_WARP
-  constexpr bool kSlotWarp = true;
-#else
-  constexpr bool kSlotWarp = ALGO == kFista;
-#endif
   const bool slot_warp = w == W - 1;
   for (int s = ow; s < SL; s += nown) prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
   // GEMM 1 multiplies by Psi^T (fista) / Psi (admm), GEMM 2 by the other
@@ -407,19 +403,9 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
   for (int tick = 0;; ++tick) {
     const int par = tick & 1;
     TMARK(0);
-    // ---- slot phase: stop rule of the last iteration, refill, momentum ----
-    // Runs inside the GEMM 1 window (no barrier between it and the GEMM): each
-    // warp handles its own slots, then joins the GEMM, which runs optimistically
-    // on every column.  The column of a slot that retires or is refilled here
-    // is garbage in this GEMM (the refill rewrites it underneath); the
-    // epilogues after the barrier replace it: admm takes the product of the
-    // fresh pixel's zero input (exactly 0) and a zero dual, so the new pixel's
-    // first iteration still runs in this tick.  fista needs Psi^T g of the new
-    // g = -y: it keeps a barrier between the slot phase and the GEMM (letting a
-    // fresh column sit one tick out instead measured 2.4% slower).
-    if constexpr (kSlotWarp) {
-    // one warp, one lane per slot: the partial sums in the tree order of the
-    // half-warp version, masks and the active count by ballots (no atomics)
+    // ---- slot phase: stop rule of the last iteration, momentum, refill ----
+    // one warp, one lane per slot: the partial sums in a fixed tree order,
+    // masks and the active count by ballots (no atomics)
     if (slot_warp) {
       const int sl_ = lane;
       const bool valid = sl_ < SL;
@@ -510,71 +496,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
         if (lane == 0) ss.need_pf[s] = 0;
         prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
       }
-    } else {
-    // two slots per pass, one per half-warp (lanes 0 and 16 lead), so the
-    // serial stop-rule / momentum code of a warp's slots runs side by side
-    for (int s0 = ow >= 0 ? ow : SL; s0 < SL; s0 += 2 * nown) {
-      const int hl = lane & 15, s = s0 + (lane >> 4) * nown;
-      const bool valid = s < SL;
-      const int st0 = valid ? ss.status[s] : kDead;
-      const bool was_active = st0 == kActive;
-      double dd = (was_active && hl < W) ? partD[hl * SL + s] : 0.0;
-      double gg = (ALGO == kAdmm && was_active && hl < W) ? partG[hl * SL + s] : 0.0;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        dd += __shfl_xor_sync(0xffffffffu, dd, o);
-        if (ALGO == kAdmm) gg += __shfl_xor_sync(0xffffffffu, gg, o);
-      }
-      if (hl == 0 && valid) {
-        ss.retired[s] = 0;
-        if (was_active) {
-          if (ALGO == kFista) ss.t[s] = ss.tn[s];
-          finish_iteration<SL>(a, ss, s, sqrt(dd), ALGO == kAdmm, gg);
-          if (ss.retired[s]) atomicOr(&ss.retmask[par], 1u << s);
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int sk = s0 + k * nown;
-        if (sk >= SL) break;
-        if (ALGO == kAdmm && ss.retired[sk] && ss.rfail[sk])   // NumericalFailure: x = 0
-          for (int n = lane; n < N; n += 32) a.x_out[ss.rpid[sk] * N + n] = 0.0;
-        if (ss.status[sk] == kEmpty) {
-          refill_slot<ALGO, SL>(a, ss, bufA, bufB, ys, r, pos, sy, sm, sk);
-          if (lane == 0) atomicOr(&ss.freshmask[par], 1u << sk);
-        }
-      }
-      if (hl == 0 && valid) {
-        const int st1 = ss.status[s];
-        if (st1 == kActive) {
-          atomicAdd(&ss.nact[par], 1);
-          ss.flag[s] = 0;
-          if (ALGO == kFista) {
-            const double t = ss.t[s];
-            const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));   // solvers.py:160-161
-            ss.tn[s] = tn;
-            ss.betan[s] = (t - 1.0) / tn;
-          }
-        } else {
-          ss.inv_l[s] = 0.0;
-          ss.thr[s] = 0.0;
-          ss.betan[s] = 0.0;
-        }
-      }
-      __syncwarp();
-    }
-    CMARK(0);
-    for (int s = ow >= 0 ? ow : SL; s < SL; s += nown)
-      if (ss.need_pf[s]) {
-        __syncwarp();
-        if (lane == 0) ss.need_pf[s] = 0;
-        prefetch_slot<ALGO, SL>(a, ss, sy, sm, s);
-      }
-    }
-    // masks of this tick's slot phase, read after the barrier that follows it
-    // (fista: the one before GEMM 1, whose input the refills wrote; admm: the
-    // one after GEMM 1)
+    // masks of this tick's slot phase (written before the barriers above)
     unsigned retm = 0u, freshm = 0u;
     bool done = false;
     auto read_masks = [&]() {
@@ -614,27 +536,19 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
           }
       }
     };
-    if (ALGO == kFista) {
-      read_masks();
-      fista_results();
-      if (done) break;
-    }
-    if (ALGO == kAdmm && kSlotWarp) {
-      read_masks();
-      if (done) break;
-    }
+    read_masks();
+    if (ALGO == kFista) fista_results();
+    if (done) break;
     CMARK(1);
     TMARK(1);
     // ---- GEMM 1 (fista: grad = Psi^T g; admm: v = Psi (z - w)) ------------
     gemm(mat1, bufA);
     TMARK(2);
-    if (ALGO == kFista || !kSlotWarp) __syncthreads();   // (admm: slot phase and) GEMM 1 of every warp done
+    // fista: its epilogue overwrites the GEMM's input; admm's writes the other
+    // buffer, so a warp runs on into its epilogue
+    if (ALGO == kFista) __syncthreads();
     TMARK(3);
     CMARK(2);
-    if (ALGO == kAdmm && !kSlotWarp) {
-      read_masks();
-      if (done) break;
-    }
 
     double part[NV];
     unsigned long long kbits = 0ull;   // fista: k-steps of this thread's nonzero x_{k+1}
@@ -791,7 +705,7 @@ __global__ void __launch_bounds__(MAXT, MINB) convex_kernel(ConvexArgs a) {
       //      residual y - A x = y - u'[mask] of this iteration's x; the last
       //      residual is y - (the u' this epilogue overwrites)[mask] ----------
       const double alpha = a.prm.alpha;
-      if (freshm) {   // slots refilled in this tick: Psi times their zero input, and a zero dual
+      if (freshm) {   // slots refilled in this tick: a zero dual (and Psi times their zero input, exactly 0)
 #pragma unroll
         for (int cb = 0; cb < CB; ++cb)
 #pragma unroll
