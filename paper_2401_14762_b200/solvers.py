@@ -14,7 +14,12 @@ reference:
   complex128 with identically zero imaginary part for real bases);
 * per-pixel masks are supported (`Dictionary.per_pixel`);
 * `time_limit` is a per-pixel device-clock budget measured from the moment a
-  pixel enters the solver; `elapsed` is that pixel's device time;
+  pixel enters the solver; `elapsed` is that pixel's device time.  With a
+  budget set (the default is 2 s, as in the reference) a gOMP / CoSaMP pixel
+  whose iterates cycle runs until the budget or `max_iter` expires, like the
+  reference's; with `time_limit=None` the kernel detects the exact state cycle
+  and jumps to the iteration cap's result (same output, `hcs_greedy.cu`), so
+  batch runs over cycling cubes (CoSaMP kappa = 33) should pass None;
 * `jobs` is accepted and ignored: pixels are scheduled by the GPU's work queue
   (multi-GPU sharding lives in `paper_2401_14762_b200.parallel`).
 """
