@@ -272,16 +272,17 @@ __device__ __forceinline__ void finish_iteration(const ConvexArgs& a, SlotState<
 }
 
 // One tick = one solver iteration of all SL slots:
-//   slot phase (stop rule on the partial sums, refill)                | barrier
-//   writeback of retired slots; GEMM 1 (reads A); epilogue 1 (writes B) | barrier
-//   GEMM 2 (reads B); epilogue 2 (writes A for the next tick)          | barrier
+//   slot phase: stop rule on the partial sums by one warp, a lane per slot | barrier
+//     refills by the slots' owner warps (only in ticks that refill)       | barrier
+//   (fista: results of retired slots;) GEMM 1 (reads A); epilogue 1 (writes B) | barrier
+//   GEMM 2 (reads B); epilogue 2 (writes A for the next tick)             | barrier
 // (admm: A = z - w, B = u'; each buffer is written only after every warp is
 // done reading it, so no barrier sits between a GEMM and its epilogue.
 // fista: A holds g, then x_{k+1}, then the next g, B holds z, two more
 // barriers.)  Per-element iterates stay in registers in the accumulator
 // layout: fista p0 = x_k; admm p1 = w (z goes to x_out every pass).
 // Residual-delta and ADMM-gap sums are reduced per warp (col_reduce) into
-// part[], summed in fixed order by the slot's owner: deterministic.
+// part[], summed in a fixed tree order by the slot warp: deterministic.
 // SL = 32: one CTA per SM, up to 16 warps of 1-2 row blocks x 4 column blocks
 // (<= 128 registers).  SL = 16: two CTAs per SM of 8 warps, up to 4 row blocks
 // x 2 column blocks each; the two CTAs drift out of phase so that one's
